@@ -1,0 +1,585 @@
+"""Host-side circuit compiler: layers -> fused gate groups -> tile passes -> register phases.
+
+This replaces the reference's per-layer applier loop (`core.py:46-72`, `grad.py:169-204`,
+one full state pass per gate position, `kernels.py:579-637`) by a schedule that streams the
+state through HBM a few times per circuit. The output is a flat int32/float64 "program"
+consumed by the sm_100a pass kernel (`csrc/lsq_kernels.cu`) through the C ABI
+(`include/layersim_cuda.h`). Everything here is pure Python/numpy, so schedule bugs are
+caught on the CPU by `tests/emulator.py`, which interprets the same program words.
+
+Vocabulary
+----------
+* wire w (reference convention: wire 0 = most significant) sits at physical bit p = n-1-w.
+* group   -- a maximal run of gates acting on exactly the same wire set (1q on w, or 2q on
+             {a,b}) with nothing else touching those wires in between. One group = one
+             local unitary U = G_s...G_1. The backward pass needs ONE coupling matrix per
+             group, M_ab = sum conj(lam_a) psi_b at the post-group point; every parameter of
+             every gate in the group is then 2 Re sum W_ab M_ab with
+             W = (G_s..G_{j+1}) dG_j (G_{j-1}..G_1) U^dag (contracted on device in fp64).
+             This generalises the reference's commuting/descending rules (grad.py:102-140).
+* pass    -- one HBM round trip over all tiles. A tile is 2^M amplitudes of one row whose
+             index bits vary over a set of M physical bits (always including the COAL lowest
+             bits, so every 2^COAL x 8 B = 128 B line is read whole). Any non-diagonal group
+             of a pass acts only on tile bits; diagonal groups may touch any bits (a bit
+             outside the tile is constant over the tile).
+* phase   -- inside a pass, each thread holds 2^R amplitudes in registers; the R register
+             bits are the only bits a non-diagonal op may touch. Phases are separated by
+             a transpose through shared memory. The first and last phase keep the COAL low
+             bits on the lanes so global loads/stores are coalesced.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .circuits import positions, slot_table, Role
+from .gates import GATE_CODE, GATE_TRAITS, GateKind
+
+COAL = 4  # low physical bits always inside a tile (16 amplitudes = one 128 B line)
+MAX_R = 5  # register bits per thread (2^5 = 32 amplitudes per vector per thread)
+MAX_M_FWD = 14
+MAX_M_BWD = 13
+ENC_FLAG = 1 << 30  # param source tag: encoding column
+FIXED_SRC = -1
+
+# op kinds (must match csrc/lsq_program.h)
+OP_U1, OP_U2, OP_DRUN = 1, 2, 3
+# diag source kinds
+SRC_NONE, SRC_REG, SRC_THREAD, SRC_NONLOCAL = 0, 1, 2, 3
+MAGIC = 0x4C535131  # "LSQ1"
+
+# program word layout sizes
+HDR_WORDS = 32
+GATE_WORDS = 8
+GROUP_WORDS = 16
+PASS_WORDS = 24
+PHASE_WORDS = 24  # 5 regbits, 16 thrbits, op0, nops, pad
+OP_WORDS = 8
+SUB_WORDS = 8
+
+
+def default_r(m: int) -> int:
+    """Register bits for a tile of M bits: 32 threads per tile when possible, <=MAX_R."""
+    if m <= 1:
+        return m
+    return max(2, min(MAX_R, m - 5))
+
+
+# ----------------------------------------------------------------------------- gates
+
+
+@dataclass
+class GateRef:
+    kind: GateKind
+    wires: tuple
+    src: list  # per parameter: FIXED_SRC | t | ENC_FLAG|e
+    fixed: list  # fixed values (same length as src)
+    layer: int
+
+    @property
+    def diag(self) -> bool:
+        return GATE_TRAITS[self.kind].diagonal
+
+    @property
+    def needs_grad(self) -> bool:
+        return any(s != FIXED_SRC for s in self.src)
+
+    @property
+    def perrow(self) -> bool:
+        return any(s != FIXED_SRC and (s & ENC_FLAG) for s in self.src)
+
+
+def flatten_gates(circuit) -> list[GateRef]:
+    """Gate list in application order with parameter sources bound to slots
+    (reference slot layout circuits.py:143-214: start + pos*k + j)."""
+    n = circuit.n
+    slots = slot_table(circuit)
+    out = []
+    for li, layer in enumerate(circuit.layers):
+        kind = GateKind(layer.gate.value)
+        k = GATE_TRAITS[kind].param_count
+        pos = positions(layer, n)
+        slot = slots[li]
+        vals = None
+        if layer.values is not None:
+            vals = np.asarray(layer.values, dtype=np.float64).reshape(len(pos), k)
+        for pi, ws in enumerate(pos):
+            src, fixed = [], []
+            for j in range(k):
+                if slot is None or slot.role is Role.FIXED:
+                    src.append(FIXED_SRC)
+                    fixed.append(float(vals[pi, j]) if vals is not None else 0.0)
+                elif slot.role is Role.TRAINABLE:
+                    src.append(slot.start + pi * k + j)
+                    fixed.append(0.0)
+                else:
+                    src.append(ENC_FLAG | (slot.start + pi * k + j))
+                    fixed.append(0.0)
+            out.append(GateRef(kind, tuple(ws), src, fixed, li))
+    return out
+
+
+# ----------------------------------------------------------------------------- groups
+
+
+@dataclass
+class Group:
+    gid: int
+    wires: tuple  # group basis order (first wire = more significant local bit)
+    gates: list = field(default_factory=list)  # list of (GateRef, reversed: bool)
+
+    @property
+    def arity(self) -> int:
+        return len(self.wires)
+
+    @property
+    def diag(self) -> bool:
+        return all(g.diag for g, _ in self.gates)
+
+    @property
+    def needs_grad(self) -> bool:
+        return any(g.needs_grad for g, _ in self.gates)
+
+    @property
+    def perrow(self) -> bool:
+        return any(g.perrow for g, _ in self.gates)
+
+    @property
+    def mat_floats(self) -> int:
+        if self.diag:
+            return 1 << self.arity  # fixed-point phase angles, one word each
+        return 8 if self.arity == 1 else 32
+
+    @property
+    def slot_floats(self) -> int:
+        if not self.needs_grad:
+            return 0
+        if self.diag:
+            return 2 << self.arity  # complex diagonal of M
+        return 8 if self.arity == 1 else 32
+
+
+def fuse_groups(gates: list[GateRef]) -> list[Group]:
+    groups: list[Group] = []
+    last: dict[int, int] = {}
+    for g in gates:
+        ws = g.wires
+        cand = last.get(ws[0])
+        ok = cand is not None and set(groups[cand].wires) == set(ws)
+        ok = ok and all(last.get(w) == cand for w in ws)
+        if ok:
+            grp = groups[cand]
+            rev = len(ws) == 2 and ws != grp.wires
+            grp.gates.append((g, rev))
+        else:
+            grp = Group(len(groups), tuple(ws), [(g, False)])
+            groups.append(grp)
+            for w in ws:
+                last[w] = grp.gid
+    return groups
+
+
+def group_preds(groups: list[Group]) -> list[set]:
+    """Dependency sets: two groups sharing a wire are ordered unless both are diagonal."""
+    preds = [set() for _ in groups]
+    last_nd: dict[int, int] = {}  # wire -> last non-diagonal group
+    diag_since: dict[int, list] = {}  # wire -> diagonal groups after it
+    for g in groups:
+        for w in g.wires:
+            if w in last_nd:
+                preds[g.gid].add(last_nd[w])
+            if not g.diag:
+                preds[g.gid].update(diag_since.get(w, []))
+        for w in g.wires:
+            if g.diag:
+                diag_since.setdefault(w, []).append(g.gid)
+            else:
+                last_nd[w] = g.gid
+                diag_since[w] = []
+    return preds
+
+
+# ----------------------------------------------------------------------------- passes
+
+
+@dataclass
+class PassPlan:
+    tile_wires: set
+    groups: list  # ordered gids
+    M: int = 0
+    R: int = 0
+    phases: list = field(default_factory=list)  # list of PhasePlan
+    local_of_phys: dict = field(default_factory=dict)
+    phys_of_local: list = field(default_factory=list)
+
+
+@dataclass
+class PhasePlan:
+    regs: list  # local bits held in registers (len R)
+    threads: list  # local bits on thread-index bits (len M-R), lane bits first
+    ops: list  # list of gids (application order)
+
+
+def _greedy_pass(order, groups, preds, done, base, M, first_forced=None):
+    S = set(base)
+    chosen, chosen_set = [], set()
+    work = 0
+    seq = list(order)
+    if first_forced is not None:
+        seq.remove(first_forced)
+        seq.insert(0, first_forced)
+    for gid in seq:
+        g = groups[gid]
+        if not preds[gid] <= (done | chosen_set):
+            continue
+        if g.diag:
+            chosen.append(gid)
+            chosen_set.add(gid)
+            continue
+        need = set(g.wires) - S
+        if len(S) + len(need) <= M:
+            S |= need
+            chosen.append(gid)
+            chosen_set.add(gid)
+            work += 1 + len(g.gates)
+    if first_forced is not None:
+        # restore program order (the forced group had no unscheduled preds)
+        pos = {gid: i for i, gid in enumerate(order)}
+        chosen.sort(key=lambda x: pos[x])
+    return S, chosen, work
+
+
+def schedule_passes(groups, n, M, seeds: int = 12) -> list[PassPlan]:
+    """Greedy tile-pass partition; tries a few seeds per pass and keeps the one that
+    schedules the most non-diagonal work."""
+    preds = group_preds(groups)
+    remaining = [g.gid for g in groups]
+    done: set = set()
+    passes = []
+    if n <= M:
+        return [PassPlan(set(range(n)), remaining, M=n)]
+    # wires at the lowest physical bits (coalescing); leave room for one 2-qubit gate
+    base = {n - 1 - p for p in range(min(COAL, max(0, M - 2)))}
+    while remaining:
+        best = _greedy_pass(remaining, groups, preds, done, base, M)
+        ready_nd = [
+            gid for gid in remaining if preds[gid] <= done and not groups[gid].diag
+        ][:seeds]
+        for gid in ready_nd[1:]:
+            cand = _greedy_pass(remaining, groups, preds, done, base, M, first_forced=gid)
+            if cand[2] > best[2]:
+                best = cand
+        S, chosen, _ = best
+        if not chosen:
+            raise RuntimeError("scheduler made no progress")
+        # fill the tile to exactly M wires with the wires needed soonest
+        if len(S) < M:
+            for gid in remaining:
+                for w in groups[gid].wires:
+                    if len(S) < M and w not in S:
+                        S.add(w)
+            for w in range(n):
+                if len(S) < M and w not in S:
+                    S.add(w)
+        passes.append(PassPlan(S, chosen, M=M))
+        done |= set(chosen)
+        cs = set(chosen)
+        remaining = [g for g in remaining if g not in cs]
+    return passes
+
+
+# ----------------------------------------------------------------------------- phases
+
+# Shared-memory XOR swizzle of the amplitude index: S(L) = L ^ h(L >> 4), h linear.
+SWZ_H = [1, 2, 4, 8, 3, 6, 12, 11, 5, 10, 7, 14, 15, 9]
+
+
+def swz_vec(local_bit: int) -> int:
+    """Contribution of local bit to the low-4 bank index of S(L)."""
+    if local_bit < 4:
+        return 1 << local_bit
+    return SWZ_H[local_bit - 4]
+
+
+def _lane_order(thread_bits, coalesced):
+    """Order thread bits so the 4 lowest lanes' swizzle vectors are independent."""
+    tb = sorted(thread_bits)
+    if coalesced:
+        return tb  # local bits 0..3 first: contiguous 128 B per half-warp
+    chosen, basis = [], []
+    rest = list(tb)
+    for b in tb:
+        if len(chosen) == 4:
+            break
+        v = swz_vec(b)
+        for e in basis:
+            v = min(v, v ^ e)
+        if v:
+            basis.append(v)
+            basis.sort(reverse=True)
+            chosen.append(b)
+            rest.remove(b)
+    return chosen + rest
+
+
+def schedule_phases(pp: PassPlan, groups, preds, n: int, R: int) -> None:
+    M = pp.M
+    phys = sorted(n - 1 - w for w in pp.tile_wires)
+    pp.phys_of_local = phys
+    pp.local_of_phys = {p: i for i, p in enumerate(phys)}
+    loc = lambda w: pp.local_of_phys[n - 1 - w]  # noqa: E731
+    coal = COAL if (M - R) >= COAL else 0
+    low = set(range(coal))
+    in_pass = set(pp.groups)
+    ext_done = set()  # groups outside this pass count as satisfied
+    remaining = list(pp.groups)
+    done: set = set()
+    phases = []
+    first = True
+    while remaining:
+        regs: set = set()
+        ops = []
+        opset = set()
+        for gid in remaining:
+            g = groups[gid]
+            if not {p for p in preds[gid] if p in in_pass} <= (done | opset):
+                continue
+            if g.diag:
+                ops.append(gid)
+                opset.add(gid)
+                continue
+            need = {loc(w) for w in g.wires} - regs
+            if first and need & low:
+                continue
+            if len(regs) + len(need) <= R:
+                regs |= need
+                ops.append(gid)
+                opset.add(gid)
+        if not ops and not first:
+            raise RuntimeError("phase scheduler made no progress")
+        phases.append([regs, ops])
+        done |= opset
+        remaining = [g for g in remaining if g not in opset]
+        first = False
+    if not phases:
+        phases.append([set(), []])
+    if coal and (phases[-1][0] & low):
+        phases.append([set(), []])
+    if coal and (phases[0][0] & low):  # cannot happen (first-phase rule) but keep it safe
+        phases.insert(0, [set(), []])
+    out = []
+    for i, (regs, ops) in enumerate(phases):
+        coalesced = coal and (i == 0 or i == len(phases) - 1)
+        regs = sorted(regs)
+        pool = [b for b in range(M) if b not in regs and not (coalesced and b in low)]
+        # pad register bits, preferring high local bits (keeps low bits on lanes)
+        for b in sorted(pool, reverse=True):
+            if len(regs) >= R:
+                break
+            regs.append(b)
+        assert len(regs) == R, (regs, R, M)
+        threads = [b for b in range(M) if b not in regs]
+        threads = _lane_order(threads, coalesced)
+        out.append(PhasePlan(regs, threads, ops))
+    pp.phases = out
+    pp.R = R
+
+
+# ----------------------------------------------------------------------------- program
+
+
+@dataclass
+class Program:
+    n: int
+    groups: list
+    passes: list
+    trainable_count: int
+    encoding_count: int
+    slot_base: dict  # gid -> global float offset of its coupling slot
+    slot_total: int
+    words: np.ndarray = None
+    fvals: np.ndarray = None
+    M: int = 0
+    gates: list = None
+
+    @property
+    def n_passes(self) -> int:
+        return len(self.passes)
+
+
+def compile_circuit(circuit, M: int | None = None, R: int | None = None) -> Program:
+    """Compile a (reference-compatible) circuit into a pass program."""
+    n = int(circuit.n)
+    gates = flatten_gates(circuit)
+    groups = fuse_groups(gates)
+    preds = group_preds(groups)
+    if M is None:
+        M = min(n, MAX_M_BWD)
+    M = min(M, n)
+    passes = schedule_passes(groups, n, M)
+    need2 = any(g.arity == 2 and not g.diag for g in groups)
+    for pp in passes:
+        r = default_r(pp.M) if R is None else min(R, pp.M)
+        if need2 and r < 2:
+            r = min(2, pp.M)
+        schedule_phases(pp, groups, preds, n, r)
+    slot_base, total = {}, 0
+    for pp in passes:
+        for gid in pp.groups:
+            g = groups[gid]
+            if g.slot_floats:
+                slot_base[gid] = total
+                total += g.slot_floats
+    T = getattr(circuit, "trainable_count", None)
+    E = getattr(circuit, "encoding_count", None)
+    if T is None:
+        from .circuits import Circuit
+
+        c2 = Circuit(circuit.n, circuit.layers)
+        T, E = c2.trainable_count, c2.encoding_count
+    prog = Program(n, groups, passes, T, E, slot_base, total, M=M, gates=gates)
+    encode(prog)
+    return prog
+
+
+def _src_word(gw, src):
+    return src
+
+
+def encode(prog: Program) -> None:
+    """Serialise the program (layout documented in include/layersim_cuda.h)."""
+    n = prog.n
+    gates_w, fvals = [], []
+    group_w = []
+    gate_index = 0
+    for g in prog.groups:
+        g0 = gate_index
+        for gate, rev in g.gates:
+            src = list(gate.src) + [FIXED_SRC] * (3 - len(gate.src))
+            fixed = list(gate.fixed) + [0.0] * (3 - len(gate.fixed))
+            foff = len(fvals)
+            fvals.extend(fixed)
+            gates_w.append([GATE_CODE[gate.kind], int(rev), src[0], src[1], src[2], foff, g.gid, len(gate.src)])
+            gate_index += 1
+        wa = g.wires[0]
+        wb = g.wires[1] if g.arity == 2 else -1
+        group_w.append(
+            [g.arity, int(g.diag), int(g.perrow), len(g.gates), g0, wa, wb,
+             prog.slot_base.get(g.gid, -1), g.slot_floats, g.mat_floats, int(g.needs_grad),
+             0, 0, 0, 0, 0]
+        )
+    pass_w, phase_w, op_w, sub_w, pgrp_w = [], [], [], [], []
+    for pi, pp in enumerate(prog.passes):
+        # per-pass shared-memory tables: group matrices, coupling slots (float offsets)
+        mat_off, slot_off = {}, {}
+        mo = so = 0
+        for gid in pp.groups:
+            g = prog.groups[gid]
+            mat_off[gid] = mo
+            mo += g.mat_floats
+            if g.slot_floats:
+                slot_off[gid] = so
+                so += g.slot_floats
+        pg0 = len(pgrp_w)
+        for gid in pp.groups:
+            pgrp_w.append([gid, mat_off[gid], slot_off.get(gid, -1), 0])
+        tile_mask = 0
+        for p in pp.phys_of_local:
+            tile_mask |= 1 << p
+        ph0 = len(phase_w)
+        first_slot = min((prog.slot_base[g] for g in pp.groups if g in prog.slot_base), default=0)
+        for ph in pp.phases:
+            op0 = len(op_w)
+            reg_of_local = {b: k for k, b in enumerate(ph.regs)}
+            ops = list(ph.ops)
+            i = 0
+            while i < len(ops):
+                g = prog.groups[ops[i]]
+                if not g.diag:
+                    if g.arity == 1:
+                        a = reg_of_local[pp.local_of_phys[n - 1 - g.wires[0]]]
+                        b = -1
+                        kind = OP_U1
+                    else:
+                        a = reg_of_local[pp.local_of_phys[n - 1 - g.wires[0]]]
+                        b = reg_of_local[pp.local_of_phys[n - 1 - g.wires[1]]]
+                        kind = OP_U2
+                    op_w.append([kind, a, b, g.gid, slot_off.get(g.gid, -1), mat_off[g.gid], 0, 0])
+                    i += 1
+                    continue
+                # maximal run of consecutive diagonal groups -> one DRUN op
+                s0 = len(sub_w)
+                while i < len(ops) and prog.groups[ops[i]].diag:
+                    gd = prog.groups[ops[i]]
+                    srcs = []
+                    for w in gd.wires:
+                        p = n - 1 - w
+                        if p in pp.local_of_phys:
+                            lb = pp.local_of_phys[p]
+                            if lb in reg_of_local:
+                                srcs.append((SRC_REG << 8) | reg_of_local[lb])
+                            else:
+                                srcs.append((SRC_THREAD << 8) | lb)
+                        else:
+                            srcs.append((SRC_NONLOCAL << 8) | p)
+                    if len(srcs) == 1:
+                        srcs.append(SRC_NONE << 8)
+                    sub_w.append([srcs[0], srcs[1], gd.gid, mat_off[gd.gid], slot_off.get(gd.gid, -1), gd.arity, 0, 0])
+                    i += 1
+                op_w.append([OP_DRUN, -1, -1, -1, -1, -1, s0, len(sub_w) - s0])
+            regs = list(ph.regs) + [0] * (MAX_R - len(ph.regs))
+            thr = list(ph.threads) + [0] * (16 - len(ph.threads))
+            phase_w.append(regs + thr + [op0, len(op_w) - op0, 0])
+        ops_lo = int(phase_w[ph0][21]) if pp.phases else len(op_w)
+        subs_lo = min((r[6] for r in op_w[ops_lo:] if r[0] == OP_DRUN), default=len(sub_w))
+        pass_w.append(
+            [pp.M, pp.R, len(pp.phases), ph0, tile_mask, len(pp.groups), pg0, mo, so,
+             first_slot, ops_lo, len(op_w) - ops_lo, subs_lo, len(sub_w) - subs_lo]
+            + [0] * (PASS_WORDS - 14)
+        )
+    hdr = [0] * HDR_WORDS
+    sections = [gates_w, group_w, pass_w, phase_w, op_w, sub_w, pgrp_w]
+    widths = [GATE_WORDS, GROUP_WORDS, PASS_WORDS, PHASE_WORDS, OP_WORDS, SUB_WORDS, 4]
+    hdr[0] = MAGIC
+    hdr[1] = 1
+    hdr[2] = n
+    hdr[3] = prog.trainable_count
+    hdr[4] = prog.encoding_count
+    hdr[5] = prog.slot_total
+    hdr[6] = len(prog.passes)
+    hdr[7] = len(prog.groups)
+    off = HDR_WORDS
+    flat = []
+    for si, (sec, wd) in enumerate(zip(sections, widths)):
+        hdr[8 + 2 * si] = off
+        hdr[9 + 2 * si] = len(sec)
+        for row in sec:
+            assert len(row) == wd, (si, row)
+            flat.extend(row)
+        off += wd * len(sec)
+    words = np.array(hdr + flat, dtype=np.int64)
+    assert words.min() >= -(2**31) and words.max() < 2**31
+    prog.words = words.astype(np.int32)
+    prog.fvals = np.asarray(fvals if fvals else [0.0], dtype=np.float64)
+
+
+def section(words: np.ndarray, idx: int, width: int) -> np.ndarray:
+    off, cnt = int(words[8 + 2 * idx]), int(words[9 + 2 * idx])
+    return words[off : off + cnt * width].reshape(cnt, width)
+
+
+SEC_GATES, SEC_GROUPS, SEC_PASSES, SEC_PHASES, SEC_OPS, SEC_SUBS, SEC_PGROUPS = range(7)
+SEC_WIDTH = [GATE_WORDS, GROUP_WORDS, PASS_WORDS, PHASE_WORDS, OP_WORDS, SUB_WORDS, 4]
+
+
+def describe(prog: Program) -> str:
+    lines = [f"n={prog.n} groups={len(prog.groups)} passes={len(prog.passes)} slot_floats={prog.slot_total}"]
+    for i, pp in enumerate(prog.passes):
+        nd = sum(1 for g in pp.groups if not prog.groups[g].diag)
+        lines.append(
+            f"  pass {i}: M={pp.M} R={pp.R} phases={len(pp.phases)} groups={len(pp.groups)} (non-diag {nd}) "
+            f"wires={sorted(pp.tile_wires)}"
+        )
+    return "\n".join(lines)

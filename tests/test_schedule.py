@@ -1,0 +1,67 @@
+"""Scheduler + program encoding, validated on the CPU by interpreting the program words
+(tests/emulator.py) and comparing with the oracle."""
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+from emulator import Emulator
+from oracle import layersim_oracle as orc
+from paper_2506_04891_b200 import schedule as S
+from paper_2506_04891_b200.configs import build_config_circuit, make_workload
+from test_oracle import rebuild_random
+
+
+def _cmp(res, ref, atol=1e-9):
+    for k in ("value", "zq", "grads", "encoding_grads"):
+        np.testing.assert_allclose(res[k], ref[k], atol=atol, err_msg=k)
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("M,R", [(6, 1), (5, 2), (4, 2), (3, 1)])
+def test_small_configs_all_tilings(cfg, M, R):
+    wl = make_workload(cfg, n=6, batch=3)
+    prog = S.compile_circuit(wl.circuit, M=M, R=R)
+    res = Emulator(prog).gradient(wl.theta, wl.x, 3, wl.weights)
+    ref = orc.gradient(wl.circuit, wl.theta, wl.x, batch=3, weights=wl.weights)
+    _cmp(res, ref)
+
+
+@pytest.mark.parametrize("c", range(6))
+@pytest.mark.parametrize("M,R", [(5, 2), (4, 2), (3, 2)])
+def test_random_circuits(c, M, R):
+    gold = load_golden("random_circuits")
+    circ = rebuild_random(gold[f"c{c}_spec"])
+    prog = S.compile_circuit(circ, M=M, R=R)
+    res = Emulator(prog).gradient(gold[f"c{c}_theta"], gold[f"c{c}_x"], 3, gold[f"c{c}_w"])
+    _cmp(res, {k[len(f"c{c}_"):]: v for k, v in gold.items() if k.startswith(f"c{c}_")})
+
+
+def test_forward_state_matches_oracle():
+    wl = make_workload(5, n=7, batch=2)
+    prog = S.compile_circuit(wl.circuit, M=5, R=2)
+    psi = Emulator(prog).forward(wl.theta, wl.x, 2)
+    ref = orc.apply_circuit(wl.circuit, wl.theta, wl.x, batch=2)
+    np.testing.assert_allclose(psi, ref, atol=1e-9)
+
+
+def test_cfg1_full_golden():
+    gold = load_golden("cfg1_full")
+    wl = make_workload(1)
+    prog = S.compile_circuit(wl.circuit)
+    res = Emulator(prog).gradient(wl.theta, wl.x, 64, wl.weights)
+    _cmp(res, gold)
+
+
+def test_program_invariants():
+    for cfg in range(1, 6):
+        prog = S.compile_circuit(build_config_circuit(cfg))
+        seen = []
+        for pp in prog.passes:
+            assert len(pp.tile_wires) == pp.M
+            seen += pp.groups
+            for i, ph in enumerate(pp.phases):
+                assert sorted(ph.regs + ph.threads) == list(range(pp.M))
+                if pp.M - pp.R >= S.COAL and i in (0, len(pp.phases) - 1):
+                    assert ph.threads[: S.COAL] == list(range(S.COAL))
+        assert sorted(seen) == list(range(len(prog.groups)))
