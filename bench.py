@@ -1,0 +1,406 @@
+#!/usr/bin/env python
+"""Benchmark: batched forward + adjoint-backward circuit evaluations per second.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
+
+One JSON line (rank 0). A step = one forward + adjoint backward of this GPU's batch
+(inputs resident in HBM) plus, for N > 1, the NCCL all-reduce of the shared-angle
+gradient. Default workload: BASELINE configs[1] (cfg2, n=16, batch 512 per GPU, weak
+scaling); --config 5 runs the 24-qubit, batch-1024 config sharded over the GPUs (strong
+scaling). `--impl reference` times the reference algorithm on the host cores (the CPU
+oracle port) on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2506_04891_b200.configs import CONFIG_NAMES, CONFIG_SHAPES, make_workload  # noqa: E402
+
+METRIC = "batched fwd+bwd circuit evals/s"
+UNIT = "evals/s"
+FALLBACK_HBM = 6650.0
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM, "fallback"
+
+
+def _dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def _workload_rows(cfg, world, rank):
+    """(workload, start, stop, global_batch, scaling) for this rank."""
+    n, b = CONFIG_SHAPES[cfg]
+    if cfg == 5:  # BASELINE: 1024 rows sharded over the GPUs
+        from paper_2506_04891_b200.distributed import shard_rows
+
+        wl = make_workload(cfg)
+        s, e = shard_rows(b, world, rank)
+        return wl, s, e, b, "strong"
+    wl = make_workload(cfg, batch=b * world)  # b rows per GPU
+    return wl, rank * b, (rank + 1) * b, b * world, "weak"
+
+
+# ------------------------------------------------------------------------------ CPU leg
+
+
+def _cpu_rows_worker(args):
+    cfg, rows, prefix = args
+    from oracle import layersim_oracle as orc
+
+    wl = make_workload(cfg, batch=max(rows) + 1)
+    out = 0
+    for r in rows:
+        c = wl.circuit
+        if prefix is not None:
+            from paper_2506_04891_b200.circuits import Circuit
+
+            c = Circuit(c.n, c.layers[:prefix])
+            th = wl.theta[: c.trainable_count]
+            orc.gradient(c, th, wl.x[r : r + 1, : c.encoding_count], batch=1, weights=wl.weights)
+        else:
+            orc.gradient(c, wl.theta, wl.x[r : r + 1], batch=1, weights=wl.weights)
+        out += 1
+    return out
+
+
+def _cpu_sample_plan(cfg):
+    """(rows, layer prefix or None, extrapolation factor, description)."""
+    n, _ = CONFIG_SHAPES[cfg]
+    ncores = os.cpu_count() or 1
+    if n <= 16:
+        rows = ncores if n == 16 else 64 * ncores
+        return rows, None, 1.0, f"{rows} full rows of cfg{cfg} (1 row per task, {ncores} processes)"
+    # n >= 20: one full row takes minutes on one core; time a layer prefix of one row per
+    # core and scale by the layer count (per-layer cost of the reference is uniform).
+    wl = make_workload(cfg, batch=1)
+    L = len(wl.circuit.layers)
+    prefix = 1 + (L - 1) // (8 if n >= 22 else 4)
+    return ncores, prefix, L / prefix, (
+        f"{ncores} rows x first {prefix}/{L} layers of cfg{cfg} (fwd+adjoint of the prefix),"
+        f" scaled by {L}/{prefix}"
+    )
+
+
+def cpu_baseline(cfg, steps=1):
+    """Oracle port (reference algorithm, complex128 numpy) on all host cores."""
+    import multiprocessing as mp
+
+    rows, prefix, scale, desc = _cpu_sample_plan(cfg)
+    ncores = os.cpu_count() or 1
+    procs = min(ncores, rows)
+    tasks = [(cfg, list(range(i, rows, procs)), prefix) for i in range(procs)]
+    ctx = mp.get_context("fork")
+    with ctx.Pool(procs) as pool:
+        times = []
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            done = sum(pool.map(_cpu_rows_worker, tasks))
+            times.append(time.perf_counter() - t0)
+    per = statistics.mean(times) * scale
+    return {"value": done / per, "unit": UNIT, "cores": procs, "kind": "port", "sample": desc,
+            "seconds_per_sample": per}
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    cfg = args.config
+    n, b = CONFIG_SHAPES[cfg]
+    import multiprocessing as mp
+
+    rows, prefix, scale, desc = _cpu_sample_plan(cfg)
+    ncores = os.cpu_count() or 1
+    procs = min(ncores, rows)
+    tasks = [(cfg, list(range(i, rows, procs)), prefix) for i in range(procs)]
+    with mp.get_context("fork").Pool(procs) as pool:
+        for _ in range(args.warmup):
+            pool.map(_cpu_rows_worker, tasks)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            pool.map(_cpu_rows_worker, tasks)
+        el = (time.perf_counter() - t0) * scale
+    value = rows * args.steps / el
+    _, _, gb, scaling = (None, None, b, "weak" if cfg != 5 else "strong")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
+        "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "c128",
+        "data": "synthetic (seeded BASELINE inputs)",
+        "config": {"workload": CONFIG_NAMES[cfg], "n_qubits": n, "global_batch": b, "sample_rows": rows},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "port", "sample": desc},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------ GPU leg
+
+
+class ClockSampler:
+    def __init__(self, gpu_indices):
+        self.idx = ",".join(str(i) for i in gpu_indices)
+        self.proc = None
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", self.idx, f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                out = ""
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            p = [x.strip() for x in l.split(",")]
+            if len(p) < 8:
+                continue
+            try:
+                sm.append(float(p[1]))
+                mx = float(p[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def _pass_vectors(prog, mode, pidx):
+    """State-vector transfers (reads + writes of one (rows, 2^n) vector) of one launch."""
+    L = len(prog.passes)
+    if mode == 0:  # forward: read psi (not for the synthesized first pass) + write psi
+        return (0 if pidx == 0 else 1) + 1
+    if mode == 1:  # turnaround: read psi (unless synthesized), write lambda (unless last)
+        return (0 if L == 1 else 1) + (1 if L > 1 else 0)
+    return 2 + (2 if pidx > 0 else 0)  # adjoint: read psi, lambda; write both unless pass 0
+
+
+def run_ours(args, world, rank, local):
+    import torch
+
+    from paper_2506_04891_b200 import gradient
+    from paper_2506_04891_b200.engine import Engine
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = args.config
+    wl, r0, r1, gbatch, scaling = _workload_rows(cfg, world, rank)
+    b = r1 - r0
+    n = wl.n
+    eng = Engine(wl.circuit, device=dev)
+    theta = torch.as_tensor(wl.theta, device=dev)
+    x = torch.as_tensor(wl.x[r0:r1], device=dev)
+    w = torch.as_tensor(wl.weights, device=dev)
+    mb = eng.micro_batch(b, 2)
+    bufs = None
+
+    def step():
+        nonlocal bufs
+        r = eng.fwd_bwd(theta, x, batch=b, weights=w, rows=False, encoding_grads=False,
+                        micro_batch=mb, buffers=bufs)
+        bufs = r["buffers"]
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.all_reduce(r["grad_sum"])
+        return r
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    barrier()
+    launches = eng.native.launch_count()
+    nchunks = (b + mb - 1) // mb
+    with ClockSampler([local] if world == 1 else list(range(world))) as clk:
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            step()
+        e1.record()
+        barrier()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = gbatch * args.steps / (ms / 1e3)
+
+    # ---- roofline: per-launch CUDA events on the engine's stream (separate profiled steps)
+    eng.native.set_profiling(True)
+    per_kernel = {}
+    for _ in range(max(2, min(args.steps, 5))):
+        eng.fwd_bwd(theta, x, batch=b, weights=w, rows=False, encoding_grads=False, micro_batch=mb,
+                    buffers=bufs)
+        for kind, t in eng.native.pass_times():
+            mode, pidx = divmod(kind, 1000)
+            vec = _pass_vectors(eng.program, mode, pidx)
+            rows_launch = mb  # every launch covers one micro-batch
+            key = "lsq_pass_kernel<M=%d,NV=%d>" % (eng.program.passes[pidx].M, 1 if mode == 0 else 2)
+            d = per_kernel.setdefault(key, {"bytes": 0.0, "ms": 0.0, "launches": 0})
+            d["bytes"] += vec * rows_launch * (8 << n)
+            d["ms"] += t
+            d["launches"] += 1
+    eng.native.set_profiling(False)
+    peak, peak_src = _peaks()
+    dom = max(per_kernel.items(), key=lambda kv: kv[1]["ms"])
+    ach = dom[1]["bytes"] / (dom[1]["ms"] / 1e3) / 1e9
+    all_b = sum(v["bytes"] for v in per_kernel.values())
+    all_ms = sum(v["ms"] for v in per_kernel.values())
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get(dom[0])
+        except Exception:
+            traffic = None
+    roofline = {
+        "bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+        "frac": round(ach / peak, 4), "traffic": traffic, "peak_source": peak_src,
+        "kernel": dom[0], "avg_launch_ms": dom[1]["ms"] / dom[1]["launches"],
+        "bytes_per_launch": dom[1]["bytes"] / dom[1]["launches"],
+        "all_pass_kernels": {"achieved": round(all_b / (all_ms / 1e3) / 1e9, 1),
+                             "frac": round(all_b / (all_ms / 1e3) / 1e9 / peak, 4),
+                             "share_of_step": round(all_ms / (ms / args.steps), 4)},
+        "per_kernel": {k: {"GBps": round(v["bytes"] / (v["ms"] / 1e3) / 1e9, 1),
+                           "ms_per_step": v["ms"] / max(2, min(args.steps, 5)),
+                           "launches_per_step": v["launches"] // max(2, min(args.steps, 5))}
+                       for k, v in per_kernel.items()},
+    }
+
+    # ---- e2e through the public API, host buffers in and out
+    x_host = np.ascontiguousarray(wl.x[r0:r1])
+    h2d = wl.theta.nbytes + x_host.nbytes + wl.weights.nbytes
+    res = None
+    for _ in range(1):
+        res = gradient(wl.circuit, wl.theta, x_host, batch=b, weights=wl.weights, device=dev)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        res = gradient(wl.circuit, wl.theta, x_host, batch=b, weights=wl.weights, device=dev)
+        if world > 1:
+            import torch.distributed as dist
+
+            gs = torch.as_tensor(res.grad_sum, device=dev)
+            dist.all_reduce(gs)
+            gs.cpu()
+    barrier()
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    d2h = res.value.nbytes + res.grads.nbytes + res.encoding_grads.nbytes + res.zq.nbytes + res.grad_sum.nbytes
+    e2e = {"value": gbatch * args.steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+           "d2h_bytes_per_step": int(d2h)}
+
+    if rank != 0:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        try:
+            cpu = cpu_baseline(cfg)
+        except Exception as e:  # pragma: no cover
+            cpu = {"value": None, "error": str(e)}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": scaling, "vs_baseline": None, "dtype": "c64 (fp32 complex; fp64 reductions)",
+        "data": "synthetic (seeded BASELINE inputs, A5 draw order)",
+        "config": {"workload": CONFIG_NAMES[cfg], "n_qubits": n, "global_batch": gbatch,
+                   "rows_per_gpu": b, "micro_batch": mb, "parallelism": f"dp{world}",
+                   "passes": len(eng.program.passes),
+                   "l2": f"working set {2 * b * (8 << n) / 2**20:.0f} MiB (psi+lambda) vs 126 MB L2"
+                         + (" -> inputs larger than L2" if 2 * b * (8 << n) > 126e6 else " (L2-resident)")},
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches * args.steps,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    world, rank, local = _dist_env()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+    else:
+        run_ours(args, world, rank, local)
+
+
+if __name__ == "__main__":
+    main()

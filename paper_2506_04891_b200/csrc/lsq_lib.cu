@@ -1,0 +1,607 @@
+// lsq_lib.cu -- C ABI of the engine (include/layersim_cuda.h): program objects, the
+// forward / forward+adjoint drivers, and the small auxiliary kernels (group tables,
+// deterministic fp64 reductions, coupling contraction).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/layersim_cuda.h"
+#include "lsq_common.cuh"
+#include "lsq_pass.cuh"
+#include "lsq_kernels.h"
+
+using namespace lsq;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+#define CUDA_TRY(expr)                                                                    \
+  do {                                                                                    \
+    cudaError_t _e = (expr);                                                              \
+    if (_e != cudaSuccess)                                                                \
+      return fail(LSQ_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));        \
+  } while (0)
+
+// ---- auxiliary kernels -----------------------------------------------------------------
+
+// shared (non per-row) group tables: 32 floats per group
+__global__ void k_group_table(const int* W, const double* fvals, const double* theta, float* gmats) {
+  const int ng = sec_cnt(W, SEC_GROUPS);
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < ng; g += gridDim.x * blockDim.x) {
+    const int* grp = W + sec_off(W, SEC_GROUPS) + g * GROUP_WORDS;
+    if (grp[GW_PERROW]) continue;
+    group_table_entry(W, g, fvals, theta, nullptr, gmats + (size_t)g * 32);
+  }
+}
+
+// Macc[b][first + f] = sum_c part[(b*cpr + c)*slotf + f]   (fixed order)
+__global__ void k_reduce_part(const double* part, int cpr, int slotf, double* macc, int slot_total,
+                              int first, int batch) {
+  const int64_t total = (int64_t)batch * slotf;
+  for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total;
+       id += (int64_t)gridDim.x * blockDim.x) {
+    const int b = (int)(id / slotf), f = (int)(id % slotf);
+    double s = 0.0;
+    const double* src = part + (size_t)b * cpr * slotf + f;
+    for (int c = 0; c < cpr; ++c) s += src[(size_t)c * slotf];
+    macc[(size_t)b * slot_total + first + f] = s;
+  }
+}
+
+// zq[b][q] and value[b] from per-CTA partials indexed by physical bit
+__global__ void k_reduce_z(const double* zpart, int cpr, int n, const double* wts, double* zq,
+                           double* value, int batch) {
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < batch; b += gridDim.x * blockDim.x) {
+    double val = 0.0;
+    for (int q = 0; q < n; ++q) {
+      const int p = n - 1 - q;
+      double s = 0.0;
+      for (int c = 0; c < cpr; ++c) s += zpart[((size_t)b * cpr + c) * (n + 1) + p];
+      if (zq) zq[(size_t)b * n + q] = s;
+      val += (wts ? wts[q] : 1.0) * s;
+    }
+    if (value) value[b] = val;
+  }
+}
+
+// per (row, group): grads of every parameter of every gate in the group,
+// g = 2 Re sum_ab W_ab M_ab,  W = (G_s..G_{j+1}) dG_j (G_{j-1}..G_1) U^dag
+__global__ void k_contract(const int* W, const double* fvals, const double* theta, const double* x,
+                           int x_stride, const double* macc, int slot_total, int batch,
+                           double* grows, int T, double* erows, int E) {
+  const int ng = sec_cnt(W, SEC_GROUPS);
+  const int64_t total = (int64_t)batch * ng;
+  const int* gates = W + sec_off(W, SEC_GATES);
+  for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total;
+       id += (int64_t)gridDim.x * blockDim.x) {
+    const int b = (int)(id / ng), gid = (int)(id % ng);
+    const int* grp = W + sec_off(W, SEC_GROUPS) + gid * GROUP_WORDS;
+    if (!grp[GW_GRAD] || grp[GW_SLOT] < 0) continue;
+    const double* xrow = x ? x + (size_t)b * x_stride : nullptr;
+    const int d = 1 << grp[GW_ARITY];
+    const double* mrow = macc + (size_t)b * slot_total + grp[GW_SLOT];
+    cd Mm[16];
+    mat_zero(Mm, d);
+    if (grp[GW_DIAG]) {
+      for (int e = 0; e < d; ++e) Mm[e * d + e] = cd{mrow[2 * e], mrow[2 * e + 1]};
+    } else {
+      for (int e = 0; e < d * d; ++e) Mm[e] = cd{mrow[2 * e], mrow[2 * e + 1]};
+    }
+    cd U[16], Ud[16], A[16], Bm[16], G[16], dG[16], Wm[16];
+    group_unitary(W, gid, fvals, theta, xrow, U);
+    mat_dag(U, Ud, d);
+    mat_eye(A, d);
+    const int ngt = grp[GW_NG];
+    for (int j = 0; j < ngt; ++j) {
+      const int* gw = gates + (grp[GW_G0] + j) * GATE_WORDS;
+      double p[3] = {0, 0, 0};
+      for (int k = 0; k < gw[7]; ++k) p[k] = gate_param(gw, k, fvals, theta, xrow);
+      gate_matrix_dev(gw[0], p, G);
+      if (d == 4 && gw[1]) mat_swap_wires(G);
+      // B = G_s ... G_{j+1}
+      mat_eye(Bm, d);
+      for (int jj = j + 1; jj < ngt; ++jj) {
+        const int* gw2 = gates + (grp[GW_G0] + jj) * GATE_WORDS;
+        double p2[3] = {0, 0, 0};
+        for (int k = 0; k < gw2[7]; ++k) p2[k] = gate_param(gw2, k, fvals, theta, xrow);
+        cd G2[16];
+        gate_matrix_dev(gw2[0], p2, G2);
+        if (d == 4 && gw2[1]) mat_swap_wires(G2);
+        mat_mul(G2, Bm, Bm, d);
+      }
+      for (int k = 0; k < gw[7]; ++k) {
+        const int s = gw[2 + k];
+        if (s == -1) continue;
+        gate_deriv_dev(gw[0], p, k, dG);
+        if (d == 4 && gw[1]) mat_swap_wires(dG);
+        mat_mul(dG, A, Wm, d);
+        mat_mul(Bm, Wm, Wm, d);
+        mat_mul(Wm, Ud, Wm, d);
+        double g = 0.0;
+        for (int e = 0; e < d * d; ++e) g += Wm[e].r * Mm[e].r - Wm[e].i * Mm[e].i;
+        g *= 2.0;
+        if (s & ENC_FLAG) {
+          if (erows) erows[(size_t)b * E + (s & ~ENC_FLAG)] = g;
+        } else {
+          if (grows) grows[(size_t)b * T + s] = g;
+        }
+      }
+      mat_mul(G, A, A, d);
+    }
+  }
+}
+
+__global__ void k_zero(double* p, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = 0.0;
+}
+
+// grad_sum[t] = sum_b grows[b][t], fixed order
+__global__ void k_sum_rows(const double* grows, int batch, int T, double* out) {
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int b = 0; b < batch; ++b) s += grows[(size_t)b * T + t];
+    out[t] = s;
+  }
+}
+
+// ---- pass kernel table (instantiated in lsq_inst.cu, one TU each) -------------------------
+using PassFn = void (*)(PassArgs);
+
+struct KEntry {
+  PassFn fn;
+  int M, R, NV, NT;
+};
+
+KEntry kernel_for(int M, int NV) {
+#define LSQ_TRY(m, nv)                                           \
+  if (M == m && NV == nv) {                                      \
+    KernelEntry e = lsq_kernel_entry_##m##_##nv();               \
+    return KEntry{(PassFn)e.fn, e.M, e.R, e.NV, e.NT};           \
+  }
+  LSQ_FOR_EACH_KERNEL(LSQ_TRY)
+#undef LSQ_TRY
+  return KEntry{nullptr, M, 0, NV, 0};
+}
+
+int pow2floor(int64_t v) {
+  int r = 1;
+  while ((int64_t)r * 2 <= v) r *= 2;
+  return r;
+}
+
+}  // namespace
+
+struct PassInfo {
+  int M, R, nph, slotf, matf, nops, nsubs, first_slot;
+  KEntry k1, k2;
+};
+
+struct lsq_program {
+  int n, T, E, npasses, ngroups, slot_total;
+  int* d_words = nullptr;
+  double* d_fvals = nullptr;
+  std::vector<int> words;
+  std::vector<PassInfo> passes;
+  int sm_count = 148;
+  bool profiling = false;
+  std::vector<cudaEvent_t> ev;  // pool: 2 events per profiled pass launch
+  int ev_used = 0;
+  std::vector<int> kinds;
+  int launches = 0;  // kernels launched by the last call
+};
+
+namespace {
+
+size_t smem_bytes(const lsq_program* P, const PassInfo& pi, int NV) {
+  const KEntry& k = NV == 1 ? pi.k1 : pi.k2;
+  const int NW = (k.NT + 31) / 32;
+  size_t b = sizeof(float2) * ((size_t)1 << pi.M);
+  b += sizeof(int) * ((size_t)pi.nph * PHASE_WORDS + (size_t)pi.nops * OP_WORDS + (size_t)pi.nsubs * SUB_WORDS + 64);
+  b += sizeof(float) * (((pi.matf + 3) & ~3) + ((NW * pi.slotf + 3) & ~3));
+  b += sizeof(double) * 34;
+  b += sizeof(float) * NW * (pi.M + 1);
+  return (b + 15) & ~(size_t)15;
+}
+
+struct Geometry {
+  int tpc, cpr;
+};
+
+Geometry geometry(const lsq_program* P, const PassInfo& pi, int batch) {
+  const int ntiles = 1 << (P->n - pi.M);
+  const int64_t total = (int64_t)batch * ntiles;
+  const int64_t target = (int64_t)P->sm_count * 8;
+  int tpc = total > target ? pow2floor(total / target) : 1;
+  if (tpc > ntiles) tpc = ntiles;
+  if (tpc > 64) tpc = 64;
+  return Geometry{tpc, ntiles / tpc};
+}
+
+struct WS {
+  float* gmats;
+  double* part;
+  double* zpart;
+  double* macc;
+  double* grows;
+  double* erows;
+  size_t bytes;
+};
+
+WS carve(const lsq_program* P, int batch, void* base) {
+  WS w{};
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += (bytes + 255) & ~(size_t)255;
+    return o;
+  };
+  size_t maxpart = 0, maxz = 0;
+  for (const auto& pi : P->passes) {
+    Geometry g = geometry(P, pi, batch);
+    maxpart = std::max(maxpart, (size_t)batch * g.cpr * pi.slotf);
+    maxz = std::max(maxz, (size_t)batch * g.cpr * (P->n + 1));
+  }
+  size_t o_g = take(sizeof(float) * 32 * (size_t)std::max(P->ngroups, 1));
+  size_t o_p = take(sizeof(double) * std::max(maxpart, (size_t)1));
+  size_t o_z = take(sizeof(double) * std::max(maxz, (size_t)1));
+  size_t o_m = take(sizeof(double) * (size_t)batch * std::max(P->slot_total, 1));
+  size_t o_gr = take(sizeof(double) * (size_t)batch * std::max(P->T, 1));
+  size_t o_er = take(sizeof(double) * (size_t)batch * std::max(P->E, 1));
+  w.bytes = off;
+  if (base) {
+    char* c = (char*)base;
+    w.gmats = (float*)(c + o_g);
+    w.part = (double*)(c + o_p);
+    w.zpart = (double*)(c + o_z);
+    w.macc = (double*)(c + o_m);
+    w.grows = (double*)(c + o_gr);
+    w.erows = (double*)(c + o_er);
+  }
+  return w;
+}
+
+int launch_pass(lsq_program* P, int pi_idx, int mode, int flags, int batch, const double* theta,
+                const double* x, int x_stride, const double* w, const float2* psi_in, float2* psi_out,
+                float2* lam, const WS& ws, cudaStream_t st) {
+  const PassInfo& pi = P->passes[pi_idx];
+  const int NV = mode == MODE_FWD ? 1 : 2;
+  const KEntry& k = NV == 1 ? pi.k1 : pi.k2;
+  if (!k.fn) return fail(LSQ_EPLAN, "no kernel instantiated for this tile size");
+  Geometry g = geometry(P, pi, batch);
+  PassArgs A{};
+  A.prog = P->d_words;
+  A.fvals = P->d_fvals;
+  A.pass = pi_idx;
+  A.mode = mode;
+  A.flags = flags;
+  A.n = P->n;
+  A.psi_in = psi_in;
+  A.psi_out = psi_out;
+  A.lam = lam;
+  A.tiles_per_cta = g.tpc;
+  A.ctas_per_row = g.cpr;
+  A.gmats = ws.gmats;
+  A.theta = theta;
+  A.x = x;
+  A.x_stride = x_stride;
+  A.wts = w;
+  A.part = ws.part;
+  A.zpart = ws.zpart;
+  const size_t sm = smem_bytes(P, pi, NV);
+  if (P->profiling) {
+    while ((int)P->ev.size() < 2 * (P->ev_used + 1)) {
+      cudaEvent_t e;
+      CUDA_TRY(cudaEventCreate(&e));
+      P->ev.push_back(e);
+    }
+    CUDA_TRY(cudaEventRecord(P->ev[2 * P->ev_used], st));
+  }
+  k.fn<<<(unsigned)((int64_t)batch * g.cpr), k.NT, sm, st>>>(A);
+  CUDA_TRY(cudaGetLastError());
+  P->launches++;
+  if (P->profiling) {
+    CUDA_TRY(cudaEventRecord(P->ev[2 * P->ev_used + 1], st));
+    P->kinds.push_back(mode * 1000 + pi_idx);
+    P->ev_used++;
+  }
+  if (pi.slotf > 0 && NV == 2) {
+    const int64_t tot = (int64_t)batch * pi.slotf;
+    const int blocks = (int)std::min<int64_t>((tot + 255) / 256, 4096);
+    k_reduce_part<<<blocks, 256, 0, st>>>(ws.part, g.cpr, pi.slotf, ws.macc, P->slot_total, pi.first_slot, batch);
+    CUDA_TRY(cudaGetLastError());
+    P->launches++;
+  }
+  return LSQ_OK;
+}
+
+int finish_grads(lsq_program* P, int batch, const double* theta, const double* x, int x_stride,
+                 const WS& ws, double* grad_rows, double* grad_sum, double* egrad_rows, cudaStream_t st) {
+  double* grows = grad_rows ? grad_rows : ws.grows;
+  double* erows = egrad_rows ? egrad_rows : (P->E ? ws.erows : nullptr);
+  if (P->T) {
+    const int64_t t = (int64_t)batch * P->T;
+    k_zero<<<(int)std::min<int64_t>((t + 255) / 256, 4096), 256, 0, st>>>(grows, t);
+    P->launches++;
+  }
+  if (erows) {
+    const int64_t t = (int64_t)batch * P->E;
+    k_zero<<<(int)std::min<int64_t>((t + 255) / 256, 4096), 256, 0, st>>>(erows, t);
+    P->launches++;
+  }
+  {
+    const int64_t tot = (int64_t)batch * P->ngroups;
+    const int blocks = (int)std::min<int64_t>((tot + 127) / 128, 8192);
+    k_contract<<<std::max(blocks, 1), 128, 0, st>>>(P->d_words, P->d_fvals, theta, x, x_stride, ws.macc,
+                                                   P->slot_total, batch, grows, P->T, erows, P->E);
+    P->launches++;
+    CUDA_TRY(cudaGetLastError());
+  }
+  if (grad_sum && P->T) {
+    k_sum_rows<<<(P->T + 127) / 128, 128, 0, st>>>(grows, batch, P->T, grad_sum);
+    P->launches++;
+    CUDA_TRY(cudaGetLastError());
+  }
+  return LSQ_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int lsq_version(void) { return 1; }
+
+const char* lsq_last_error(void) { return g_err.c_str(); }
+
+int lsq_device_info(int device, char* buf, int buflen) {
+  cudaDeviceProp p;
+  CUDA_TRY(cudaGetDeviceProperties(&p, device));
+  int drv = 0;
+  cudaDriverGetVersion(&drv);
+  snprintf(buf, buflen, "%s|%d|%d.%d|%d", p.name, p.multiProcessorCount, p.major, p.minor, drv);
+  return LSQ_OK;
+}
+
+int lsq_program_create(const int32_t* words, int64_t n_words, const double* fvals, int64_t n_fvals,
+                       lsq_program** out) {
+  if (!words || n_words < HDR_WORDS || !out) return fail(LSQ_EINVAL, "bad program words");
+  if (words[0] != MAGIC) return fail(LSQ_EINVAL, "program magic mismatch");
+  if (words[1] != 1) return fail(LSQ_EPLAN, "program version mismatch");
+  auto* P = new lsq_program();
+  P->words.assign(words, words + n_words);
+  const int* W = P->words.data();
+  P->n = W[2];
+  P->T = W[3];
+  P->E = W[4];
+  P->slot_total = W[5];
+  P->npasses = W[6];
+  P->ngroups = W[7];
+  if (P->n < 1 || P->n > 30) {
+    delete P;
+    return fail(LSQ_EINVAL, "n out of range (1..30)");
+  }
+  for (int s = 0; s < 7; ++s) {
+    if (sec_off(W, s) < HDR_WORDS || sec_off(W, s) > n_words) {
+      delete P;
+      return fail(LSQ_EINVAL, "corrupt program section table");
+    }
+  }
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&P->sm_count, cudaDevAttrMultiProcessorCount, dev);
+  for (int i = 0; i < P->npasses; ++i) {
+    const int* pw = W + sec_off(W, SEC_PASSES) + i * PASS_WORDS;
+    PassInfo pi{};
+    pi.M = pw[PW_M];
+    pi.R = pw[PW_R];
+    pi.nph = pw[PW_NPH];
+    pi.slotf = pw[PW_SLOTF];
+    pi.matf = pw[PW_MATF];
+    pi.nops = pw[PW_OPN];
+    pi.nsubs = pw[PW_SUBN];
+    pi.first_slot = pw[PW_FIRSTSLOT];
+    pi.k1 = kernel_for(pi.M, 1);
+    pi.k2 = kernel_for(pi.M, 2);
+    if (!pi.k1.fn || pi.k1.R != pi.R) {
+      delete P;
+      return fail(LSQ_EPLAN, "pass " + std::to_string(i) + ": no kernel for M=" + std::to_string(pi.M) +
+                                 " R=" + std::to_string(pi.R));
+    }
+    P->passes.push_back(pi);
+    for (int NV = 1; NV <= 2; ++NV) {
+      const KEntry& k = NV == 1 ? pi.k1 : pi.k2;
+      if (!k.fn) continue;
+      size_t sm = smem_bytes(P, pi, NV);
+      cudaError_t e = cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      if (e != cudaSuccess) {
+        delete P;
+        return fail(LSQ_ECUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+      }
+    }
+  }
+  cudaError_t e1 = cudaMalloc(&P->d_words, sizeof(int) * n_words);
+  cudaError_t e2 = cudaMalloc(&P->d_fvals, sizeof(double) * std::max<int64_t>(n_fvals, 1));
+  if (e1 != cudaSuccess || e2 != cudaSuccess) {
+    delete P;
+    return fail(LSQ_ECUDA, "cudaMalloc failed for program tables");
+  }
+  cudaMemcpy(P->d_words, words, sizeof(int) * n_words, cudaMemcpyHostToDevice);
+  if (n_fvals > 0) cudaMemcpy(P->d_fvals, fvals, sizeof(double) * n_fvals, cudaMemcpyHostToDevice);
+  CUDA_TRY(cudaGetLastError());
+  *out = P;
+  return LSQ_OK;
+}
+
+void lsq_program_destroy(lsq_program* P) {
+  if (!P) return;
+  for (auto e : P->ev) cudaEventDestroy(e);
+  cudaFree(P->d_words);
+  cudaFree(P->d_fvals);
+  delete P;
+}
+
+int lsq_program_info(const lsq_program* P, int64_t* o) {
+  if (!P || !o) return fail(LSQ_EINVAL, "null argument");
+  o[0] = P->n; o[1] = P->T; o[2] = P->E; o[3] = P->npasses; o[4] = P->ngroups; o[5] = P->slot_total;
+  o[6] = P->sm_count; o[7] = 0;
+  return LSQ_OK;
+}
+
+int64_t lsq_workspace_bytes(const lsq_program* P, int batch) {
+  if (!P || batch < 1) return -1;
+  return (int64_t)carve(P, batch, nullptr).bytes;
+}
+
+int lsq_set_profiling(lsq_program* P, int on) {
+  if (!P) return fail(LSQ_EINVAL, "null program");
+  P->profiling = on != 0;
+  return LSQ_OK;
+}
+
+int lsq_last_pass_times(const lsq_program* P, float* ms, int cap, int* kinds) {
+  if (!P) return -1;
+  const int n = P->ev_used;
+  if (n > 0 && cudaEventSynchronize(P->ev[2 * n - 1]) != cudaSuccess) return -1;
+  for (int i = 0; i < n && i < cap; ++i) {
+    float t = 0.f;
+    cudaEventElapsedTime(&t, P->ev[2 * i], P->ev[2 * i + 1]);
+    if (ms) ms[i] = t;
+    if (kinds) kinds[i] = P->kinds[i];
+  }
+  return n;
+}
+
+int lsq_last_launch_count(const lsq_program* P) { return P ? P->launches : -1; }
+
+int lsq_forward(const lsq_program* Pc, int batch, const double* theta, const double* x, int x_stride,
+                const double* w, const void* psi_in, void* psi_out, double* zq, double* value,
+                void* workspace, void* stream) {
+  auto* P = const_cast<lsq_program*>(Pc);
+  if (!P || batch < 1 || !psi_out || !workspace) return fail(LSQ_EINVAL, "null argument");
+  if (P->T && !theta) return fail(LSQ_EINVAL, "circuit has trainable parameters but none given");
+  if (P->E && !x) return fail(LSQ_EINVAL, "circuit has encoding parameters but none given");
+  cudaStream_t st = (cudaStream_t)stream;
+  WS ws = carve(P, batch, workspace);
+  P->ev_used = 0;
+  P->kinds.clear();
+  P->launches = 0;
+  k_group_table<<<std::max(1, (P->ngroups + 127) / 128), 128, 0, st>>>(P->d_words, P->d_fvals, theta, ws.gmats);
+  P->launches++;
+  CUDA_TRY(cudaGetLastError());
+  const float2* src = (const float2*)psi_in;
+  float2* dst = (float2*)psi_out;
+  const bool want_z = zq || value;
+  if (P->npasses == 0) return fail(LSQ_EPLAN, "empty program");
+  for (int i = 0; i < P->npasses; ++i) {
+    int flags = F_STORE_PSI;
+    if (i == 0 && !src) flags |= F_SYNTH;
+    if (i == P->npasses - 1 && want_z) flags |= F_ZPART;
+    const float2* in = (i == 0) ? src : dst;
+    int rc = launch_pass(P, i, MODE_FWD, flags, batch, theta, x, x_stride, w, in ? in : dst, dst, nullptr, ws, st);
+    if (rc) return rc;
+  }
+  if (want_z) {
+    Geometry g = geometry(P, P->passes.back(), batch);
+    k_reduce_z<<<(batch + 127) / 128, 128, 0, st>>>(ws.zpart, g.cpr, P->n, w, zq, value, batch);
+    P->launches++;
+    CUDA_TRY(cudaGetLastError());
+  }
+  return LSQ_OK;
+}
+
+int lsq_fwd_bwd(const lsq_program* Pc, int batch, const double* theta, const double* x, int x_stride,
+                const double* w, void* psi_v, void* lam_v, double* zq, double* value, double* grad_rows,
+                double* grad_sum, double* egrad_rows, void* workspace, void* stream) {
+  auto* P = const_cast<lsq_program*>(Pc);
+  if (!P || batch < 1 || !psi_v || !lam_v || !workspace) return fail(LSQ_EINVAL, "null argument");
+  if (P->T && !theta) return fail(LSQ_EINVAL, "circuit has trainable parameters but none given");
+  if (P->E && !x) return fail(LSQ_EINVAL, "circuit has encoding parameters but none given");
+  if (P->npasses == 0) return fail(LSQ_EPLAN, "empty program");
+  cudaStream_t st = (cudaStream_t)stream;
+  WS ws = carve(P, batch, workspace);
+  P->ev_used = 0;
+  P->kinds.clear();
+  P->launches = 0;
+  float2* psi = (float2*)psi_v;
+  float2* lam = (float2*)lam_v;
+  k_group_table<<<std::max(1, (P->ngroups + 127) / 128), 128, 0, st>>>(P->d_words, P->d_fvals, theta, ws.gmats);
+  P->launches++;
+  CUDA_TRY(cudaGetLastError());
+  const int64_t mtot = (int64_t)batch * std::max(P->slot_total, 1);
+  k_zero<<<(int)std::min<int64_t>((mtot + 255) / 256, 4096), 256, 0, st>>>(ws.macc, mtot);
+  P->launches++;
+  const int L = P->npasses;
+  for (int i = 0; i < L - 1; ++i) {
+    int flags = F_STORE_PSI | (i == 0 ? F_SYNTH : 0);
+    int rc = launch_pass(P, i, MODE_FWD, flags, batch, theta, x, x_stride, w, psi, psi, nullptr, ws, st);
+    if (rc) return rc;
+  }
+  {
+    int flags = (L == 1 ? F_SYNTH : 0) | (L > 1 ? F_STORE_LAM : 0);
+    int rc = launch_pass(P, L - 1, MODE_TURN, flags, batch, theta, x, x_stride, w, psi, psi, lam, ws, st);
+    if (rc) return rc;
+    Geometry g = geometry(P, P->passes[L - 1], batch);
+    k_reduce_z<<<(batch + 127) / 128, 128, 0, st>>>(ws.zpart, g.cpr, P->n, w, zq, value, batch);
+    P->launches++;
+    CUDA_TRY(cudaGetLastError());
+  }
+  for (int i = L - 2; i >= 0; --i) {
+    int flags = i > 0 ? (F_STORE_PSI | F_STORE_LAM) : 0;
+    int rc = launch_pass(P, i, MODE_BWD, flags, batch, theta, x, x_stride, w, psi, psi, lam, ws, st);
+    if (rc) return rc;
+  }
+  return finish_grads(P, batch, theta, x, x_stride, ws, grad_rows, grad_sum, egrad_rows, st);
+}
+
+int lsq_bwd_from_state(const lsq_program* Pc, int batch, const double* theta, const double* x,
+                       int x_stride, const double* w, const void* final_state, void* psi_v, void* lam_v,
+                       double* zq, double* value, double* grad_rows, double* grad_sum,
+                       double* egrad_rows, void* workspace, void* stream) {
+  auto* P = const_cast<lsq_program*>(Pc);
+  if (!P || batch < 1 || !final_state || !psi_v || !lam_v || !workspace)
+    return fail(LSQ_EINVAL, "null argument");
+  if (P->T && !theta) return fail(LSQ_EINVAL, "circuit has trainable parameters but none given");
+  if (P->E && !x) return fail(LSQ_EINVAL, "circuit has encoding parameters but none given");
+  if (P->npasses == 0) return fail(LSQ_EPLAN, "empty program");
+  cudaStream_t st = (cudaStream_t)stream;
+  WS ws = carve(P, batch, workspace);
+  P->ev_used = 0;
+  P->kinds.clear();
+  P->launches = 0;
+  float2* psi = (float2*)psi_v;
+  float2* lam = (float2*)lam_v;
+  k_group_table<<<std::max(1, (P->ngroups + 127) / 128), 128, 0, st>>>(P->d_words, P->d_fvals, theta, ws.gmats);
+  P->launches++;
+  CUDA_TRY(cudaGetLastError());
+  const int64_t mtot = (int64_t)batch * std::max(P->slot_total, 1);
+  k_zero<<<(int)std::min<int64_t>((mtot + 255) / 256, 4096), 256, 0, st>>>(ws.macc, mtot);
+  P->launches++;
+  const int L = P->npasses;
+  {
+    int flags = F_NOFWD | F_STORE_LAM | F_STORE_PSI;
+    int rc = launch_pass(P, L - 1, MODE_TURN, flags, batch, theta, x, x_stride, w,
+                         (const float2*)final_state, psi, lam, ws, st);
+    if (rc) return rc;
+    Geometry g = geometry(P, P->passes[L - 1], batch);
+    k_reduce_z<<<(batch + 127) / 128, 128, 0, st>>>(ws.zpart, g.cpr, P->n, w, zq, value, batch);
+    P->launches++;
+    CUDA_TRY(cudaGetLastError());
+  }
+  for (int i = L - 2; i >= 0; --i) {
+    int flags = i > 0 ? (F_STORE_PSI | F_STORE_LAM) : 0;
+    int rc = launch_pass(P, i, MODE_BWD, flags, batch, theta, x, x_stride, w, psi, psi, lam, ws, st);
+    if (rc) return rc;
+  }
+  return finish_grads(P, batch, theta, x, x_stride, ws, grad_rows, grad_sum, egrad_rows, st);
+}
+
+}  // extern "C"

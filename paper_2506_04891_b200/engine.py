@@ -1,0 +1,259 @@
+"""Device engine: a compiled circuit program bound to a CUDA device.
+
+Owns the immutable native program (`lsq_program_create`), the device workspace and the
+state buffers (torch complex64 tensors, i.e. float2 rows of 2^n amplitudes), and runs the
+forward / forward+adjoint drivers of the C ABI on torch's current stream. Rows are
+processed in micro-batches when psi+lambda for the whole batch would not fit in HBM
+(SURVEY §7.4 H5); the shared-angle gradient is summed over micro-batches in a fixed order.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _native
+from .errors import CapacityError
+from .schedule import compile_circuit
+
+_STATE_FRACTION = 0.6  # of free device memory usable for psi + lambda
+
+
+def _ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _dev_f64(a, device, shape=None):
+    if a is None:
+        return None
+    if isinstance(a, torch.Tensor):
+        t = a.detach().to(device=device, dtype=torch.float64)
+    else:
+        t = torch.as_tensor(np.asarray(a, dtype=np.float64), device=device)
+    t = t.contiguous()
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise ValueError(f"parameter shape {tuple(t.shape)} != {tuple(shape)}")
+    return t
+
+
+class NativeProgram:
+    """RAII wrapper of an lsq_program on one device."""
+
+    def __init__(self, prog, device: torch.device):
+        _native.require_cuda()
+        self.prog = prog
+        self.device = device
+        lib = _native.lib()
+        words = np.ascontiguousarray(prog.words, dtype=np.int32)
+        fvals = np.ascontiguousarray(prog.fvals, dtype=np.float64)
+        h = ctypes.c_void_p()
+        with torch.cuda.device(device):
+            _native.check(
+                lib.lsq_program_create(
+                    words.ctypes.data, words.size, fvals.ctypes.data, fvals.size, ctypes.byref(h)
+                )
+            )
+        self.handle = h
+        self._ws = {}
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            try:
+                _native.lib().lsq_program_destroy(h)
+            except Exception:
+                pass
+            self.handle = None
+
+    def workspace(self, batch: int) -> torch.Tensor:
+        ws = self._ws.get(batch)
+        if ws is None:
+            nbytes = int(_native.lib().lsq_workspace_bytes(self.handle, batch))
+            if nbytes < 0:
+                raise ValueError("invalid batch for workspace")
+            ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
+            self._ws = {batch: ws}  # keep one size cached
+        return ws
+
+    def set_profiling(self, on: bool):
+        _native.check(_native.lib().lsq_set_profiling(self.handle, int(on)))
+
+    def pass_times(self):
+        cap = 4096
+        ms = (ctypes.c_float * cap)()
+        kinds = (ctypes.c_int * cap)()
+        n = _native.lib().lsq_last_pass_times(self.handle, ms, cap, kinds)
+        return [(int(kinds[i]), float(ms[i])) for i in range(min(n, cap))]
+
+    def launch_count(self) -> int:
+        return int(_native.lib().lsq_last_launch_count(self.handle))
+
+
+class Engine:
+    """A circuit compiled for the device; the object behind the drop-in API."""
+
+    def __init__(self, circuit, M: int | None = None, R: int | None = None, device=None):
+        self.device = torch.device(device if device is not None else "cuda")
+        if self.device.type != "cuda":
+            raise ValueError("the engine runs on CUDA devices only")
+        self.circuit = circuit
+        self.n = int(circuit.n)
+        self.program = compile_circuit(circuit, M=M, R=R)
+        self.native = NativeProgram(self.program, self.device)
+        self.T = self.program.trainable_count
+        self.E = self.program.encoding_count
+
+    # -- helpers ---------------------------------------------------------------------------
+    def _stream(self):
+        return ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def _params(self, trainable, encoding, weights, batch):
+        th = _dev_f64(trainable, self.device, (self.T,)) if self.T else None
+        if self.T and th is None:
+            raise ValueError("circuit has trainable parameters but none given")
+        x = None
+        if self.E:
+            if encoding is None:
+                raise ValueError("circuit has encoding parameters but none given")
+            x = _dev_f64(encoding, self.device)
+            if x.ndim != 2 or x.shape != (batch, self.E):
+                raise ValueError(f"encoding shape {tuple(x.shape)} != ({batch}, {self.E})")
+        w = _dev_f64(weights, self.device, (self.n,)) if weights is not None else None
+        return th, x, w
+
+    def row_bytes(self, nvec: int) -> int:
+        return nvec * (8 << self.n)
+
+    def micro_batch(self, batch: int, nvec: int) -> int:
+        free, _ = torch.cuda.mem_get_info(self.device)
+        cap = int(free * _STATE_FRACTION) // self.row_bytes(nvec)
+        if cap < 1:
+            raise CapacityError(
+                f"one row of 2^{self.n} amplitudes x {nvec} vectors does not fit in device memory"
+            )
+        return min(batch, cap)
+
+    # -- forward ----------------------------------------------------------------------------
+    def forward(self, trainable=None, encoding=None, state=None, batch=None, weights=None, want_z=False):
+        """Evolve `state` ((B, 2^n) complex64 CUDA tensor, or None = |0..0> with `batch` rows)
+        through the circuit into a NEW tensor. Returns (psi, zq, value)."""
+        if state is not None:
+            if not isinstance(state, torch.Tensor) or state.dtype != torch.complex64:
+                raise ValueError("state must be a complex64 torch tensor")
+            if state.device != self.device:
+                state = state.to(self.device)
+            state = state.contiguous()
+            batch = state.shape[0]
+            if state.shape[1] != (1 << self.n):
+                raise ValueError(f"state has {state.shape[1]} amplitudes, expected 2^{self.n}")
+        if batch is None or batch < 1:
+            raise ValueError("batch must be positive")
+        th, x, w = self._params(trainable, encoding, weights, batch)
+        out = torch.empty((batch, 1 << self.n), dtype=torch.complex64, device=self.device)
+        zq = torch.empty((batch, self.n), dtype=torch.float64, device=self.device) if want_z else None
+        val = torch.empty((batch,), dtype=torch.float64, device=self.device) if want_z else None
+        lib = _native.lib()
+        mb = batch  # output buffer is the full batch already; process in one call
+        ws = self.native.workspace(mb)
+        _native.check(
+            lib.lsq_forward(
+                self.native.handle, batch, _ptr(th), _ptr(x), self.E, _ptr(w), _ptr(state),
+                out.data_ptr(), _ptr(zq), _ptr(val), ws.data_ptr(), self._stream(),
+            )
+        )
+        return out, zq, val
+
+    # -- forward + adjoint ------------------------------------------------------------------------
+    def fwd_bwd(self, trainable=None, encoding=None, batch=1, weights=None, rows=True,
+                encoding_grads=True, micro_batch=None, buffers=None):
+        """Forward from |0..0> plus adjoint backward. Returns a dict of CUDA tensors:
+        value (B,), zq (B,n), grads (B,T) if rows, grad_sum (T,), encoding_grads (B,E)."""
+        th, x, w = self._params(trainable, encoding, weights, batch)
+        mb = micro_batch or self.micro_batch(batch, 2)
+        dev = self.device
+        f64 = dict(dtype=torch.float64, device=dev)
+        value = torch.empty((batch,), **f64)
+        zq = torch.empty((batch, self.n), **f64)
+        grows = torch.empty((batch, self.T), **f64) if (rows and self.T) else None
+        erows = torch.empty((batch, self.E), **f64) if (encoding_grads and self.E) else None
+        nchunk = (batch + mb - 1) // mb
+        gparts = torch.zeros((nchunk, max(self.T, 1)), **f64)
+        if buffers is not None and buffers[0].shape[0] >= mb:
+            psi, lam = buffers
+        else:
+            psi = torch.empty((mb, 1 << self.n), dtype=torch.complex64, device=dev)
+            lam = torch.empty_like(psi)
+        ws = self.native.workspace(mb)
+        lib = _native.lib()
+        for c in range(nchunk):
+            r0 = c * mb
+            b = min(mb, batch - r0)
+            xc = x[r0 : r0 + b] if x is not None else None
+            _native.check(
+                lib.lsq_fwd_bwd(
+                    self.native.handle, b, _ptr(th), _ptr(xc), self.E, _ptr(w),
+                    psi.data_ptr(), lam.data_ptr(), zq[r0].data_ptr(), value[r0].data_ptr(),
+                    grows[r0].data_ptr() if grows is not None else None,
+                    gparts[c].data_ptr() if self.T else None,
+                    erows[r0].data_ptr() if erows is not None else None,
+                    ws.data_ptr(), self._stream(),
+                )
+            )
+        gsum = gparts.sum(dim=0)[: self.T] if nchunk > 1 else gparts[0, : self.T]
+        return {"value": value, "zq": zq, "grads": grows, "grad_sum": gsum, "encoding_grads": erows,
+                "buffers": (psi, lam)}
+
+    def backward_from_state(self, trainable, encoding, final_state, weights=None):
+        """Adjoint sweep from a given final state (reference backward_sweep)."""
+        if not isinstance(final_state, torch.Tensor) or final_state.dtype != torch.complex64:
+            raise ValueError("final state must be a complex64 torch tensor")
+        final_state = final_state.to(self.device).contiguous()
+        batch = final_state.shape[0]
+        th, x, w = self._params(trainable, encoding, weights, batch)
+        f64 = dict(dtype=torch.float64, device=self.device)
+        value = torch.empty((batch,), **f64)
+        zq = torch.empty((batch, self.n), **f64)
+        grows = torch.empty((batch, max(self.T, 1)), **f64)
+        erows = torch.empty((batch, max(self.E, 1)), **f64)
+        gsum = torch.empty((max(self.T, 1),), **f64)
+        psi = torch.empty_like(final_state)
+        lam = torch.empty_like(final_state)
+        ws = self.native.workspace(batch)
+        _native.check(
+            _native.lib().lsq_bwd_from_state(
+                self.native.handle, batch, _ptr(th), _ptr(x), self.E, _ptr(w), final_state.data_ptr(),
+                psi.data_ptr(), lam.data_ptr(), zq.data_ptr(), value.data_ptr(),
+                grows.data_ptr() if self.T else None, gsum.data_ptr() if self.T else None,
+                erows.data_ptr() if self.E else None, ws.data_ptr(), self._stream(),
+            )
+        )
+        return {"value": value, "zq": zq, "grads": grows[:, : self.T], "grad_sum": gsum[: self.T],
+                "encoding_grads": erows[:, : self.E]}
+
+
+_CACHE: dict = {}
+
+
+def engine_for(circuit, device=None, M=None, R=None) -> Engine:
+    """Cached Engine per (circuit layers, n, tiling, device)."""
+    dev = torch.device(device if device is not None else "cuda")
+    if dev.type == "cuda" and dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    key = (_circuit_key(circuit), M, R, str(dev))
+    eng = _CACHE.get(key)
+    if eng is None:
+        eng = Engine(circuit, M=M, R=R, device=dev)
+        _CACHE[key] = eng
+    return eng
+
+
+def _circuit_key(circuit):
+    layers = []
+    for l in circuit.layers:
+        layers.append(
+            (l.gate.value, l.pattern.kind.value, tuple(map(tuple, l.pattern.wires)),
+             None if l.role is None else l.role.value, l.values)
+        )
+    return (int(circuit.n), tuple(layers))

@@ -287,6 +287,8 @@ def schedule_passes(groups, n, M, seeds: int = 12) -> list[PassPlan]:
         done |= set(chosen)
         cs = set(chosen)
         remaining = [g for g in remaining if g not in cs]
+    if not passes:  # empty circuit: one pass over the lowest M bits (observables only)
+        passes.append(PassPlan({n - 1 - p for p in range(M)}, [], M=M))
     return passes
 
 
