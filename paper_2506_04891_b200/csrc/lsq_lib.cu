@@ -6,6 +6,8 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -211,6 +213,21 @@ size_t smem_bytes(const lsq_program* P, const PassInfo& pi, int NV) {
   b += sizeof(double) * 34;
   b += sizeof(float) * NW * (pi.M + 1);
   return (b + 15) & ~(size_t)15;
+}
+
+// The dynamic shared-memory opt-in is a per-kernel-function attribute shared by every
+// program in the process: only ever raise it.
+std::mutex g_smem_mu;
+std::map<const void*, size_t> g_smem_max;
+
+int ensure_smem(PassFn fn, size_t bytes) {
+  std::lock_guard<std::mutex> lock(g_smem_mu);
+  size_t& cur = g_smem_max[(const void*)fn];
+  if (bytes <= cur) return LSQ_OK;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e != cudaSuccess) return fail(LSQ_ECUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+  cur = bytes;
+  return LSQ_OK;
 }
 
 struct Geometry {
@@ -420,11 +437,10 @@ int lsq_program_create(const int32_t* words, int64_t n_words, const double* fval
     for (int NV = 1; NV <= 2; ++NV) {
       const KEntry& k = NV == 1 ? pi.k1 : pi.k2;
       if (!k.fn) continue;
-      size_t sm = smem_bytes(P, pi, NV);
-      cudaError_t e = cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      if (e != cudaSuccess) {
+      int rc = ensure_smem(k.fn, smem_bytes(P, pi, NV));
+      if (rc) {
         delete P;
-        return fail(LSQ_ECUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+        return rc;
       }
     }
   }

@@ -1,0 +1,53 @@
+"""The C-ABI library loads on the CPU host and exports every symbol include/*.h declares
+(no compute calls without a GPU)."""
+
+import ctypes
+import glob
+import os
+import re
+
+import pytest
+
+from conftest import ROOT
+from paper_2506_04891_b200 import _native
+
+
+def declared_symbols():
+    syms = set()
+    for h in glob.glob(os.path.join(ROOT, "include", "*.h")):
+        text = open(h).read()
+        text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+        syms |= set(re.findall(r"\b(lsq_\w+)\s*\(", text))
+    return syms
+
+
+def test_header_declares_entry_points():
+    syms = declared_symbols()
+    for s in ("lsq_program_create", "lsq_forward", "lsq_fwd_bwd", "lsq_bwd_from_state", "lsq_last_error"):
+        assert s in syms
+
+
+@pytest.mark.skipif(not os.path.exists(_native.LIB_PATH), reason="library not built (run build())")
+def test_library_exports_every_declared_symbol():
+    lib = ctypes.CDLL(_native.LIB_PATH)
+    missing = [s for s in sorted(declared_symbols()) if not hasattr(lib, s)]
+    assert not missing, missing
+    assert set(_native.EXPORTS) <= declared_symbols()
+    loaded = _native.load_library()
+    assert loaded.lsq_version() == 1
+
+
+def test_status_codes_map_to_reference_exceptions():
+    if not os.path.exists(_native.LIB_PATH):
+        pytest.skip("library not built")
+    from paper_2506_04891_b200.errors import CapacityError, PlanMismatchError
+
+    _native.load_library()
+    with pytest.raises(ValueError):
+        _native.check(1)
+    with pytest.raises(PlanMismatchError):
+        _native.check(2)
+    with pytest.raises(CapacityError):
+        _native.check(3)
+    with pytest.raises(RuntimeError):
+        _native.check(4)
