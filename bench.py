@@ -232,7 +232,7 @@ def run_ours(args, world, rank, local):
     wl, r0, r1, gbatch, scaling = _workload_rows(cfg, world, rank)
     b = r1 - r0
     n = wl.n
-    eng = Engine(wl.circuit, device=dev)
+    eng = Engine(wl.circuit, device=dev, M=args.M, R=args.R)
     theta = torch.as_tensor(wl.theta, device=dev)
     x = torch.as_tensor(wl.x[r0:r1], device=dev)
     w = torch.as_tensor(wl.weights, device=dev)
@@ -282,7 +282,8 @@ def run_ours(args, world, rank, local):
     # ---- roofline: per-launch CUDA events on the engine's stream (separate profiled steps)
     eng.native.set_profiling(True)
     per_kernel = {}
-    for _ in range(max(2, min(args.steps, 5))):
+    nprof = max(2, min(args.steps, 5))
+    for _ in range(nprof):
         eng.fwd_bwd(theta, x, batch=b, weights=w, rows=False, encoding_grads=False, micro_batch=mb,
                     buffers=bufs)
         for kind, t in eng.native.pass_times():
@@ -314,10 +315,10 @@ def run_ours(args, world, rank, local):
         "bytes_per_launch": dom[1]["bytes"] / dom[1]["launches"],
         "all_pass_kernels": {"achieved": round(all_b / (all_ms / 1e3) / 1e9, 1),
                              "frac": round(all_b / (all_ms / 1e3) / 1e9 / peak, 4),
-                             "share_of_step": round(all_ms / (ms / args.steps), 4)},
+                             "share_of_step": round((all_ms / nprof) / (ms / args.steps), 4)},
         "per_kernel": {k: {"GBps": round(v["bytes"] / (v["ms"] / 1e3) / 1e9, 1),
-                           "ms_per_step": v["ms"] / max(2, min(args.steps, 5)),
-                           "launches_per_step": v["launches"] // max(2, min(args.steps, 5))}
+                           "ms_per_step": v["ms"] / nprof,
+                           "launches_per_step": v["launches"] // nprof}
                        for k, v in per_kernel.items()},
     }
 
@@ -369,7 +370,8 @@ def run_ours(args, world, rank, local):
         "data": "synthetic (seeded BASELINE inputs, A5 draw order)",
         "config": {"workload": CONFIG_NAMES[cfg], "n_qubits": n, "global_batch": gbatch,
                    "rows_per_gpu": b, "micro_batch": mb, "parallelism": f"dp{world}",
-                   "passes": len(eng.program.passes),
+                   "passes": len(eng.program.passes), "tile_bits": eng.program.passes[0].M,
+                   "reg_bits": eng.program.passes[0].R, "variant": eng.variant,
                    "l2": f"working set {2 * b * (8 << n) / 2**20:.0f} MiB (psi+lambda) vs 126 MB L2"
                          + (" -> inputs larger than L2" if 2 * b * (8 << n) > 126e6 else " (L2-resident)")},
         "roofline": roofline,
@@ -394,6 +396,8 @@ def main():
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--M", type=int, default=None, help="tile bits per pass (default: planner/engine)")
+    ap.add_argument("--R", type=int, default=None, help="register bits per thread")
     args = ap.parse_args()
     world, rank, local = _dist_env()
     if args.impl == "reference":

@@ -1,0 +1,587 @@
+"""Per-circuit CUDA code generation: one straight-line sm_100a kernel per (pass, mode).
+
+The generic pass kernel (`csrc/lsq_pass.cuh`) interprets the op words at run time; its
+dispatch over runtime register indices makes the compiler copy the whole 64-register
+amplitude tile at every op (ncu: 54% of executed instructions were MOVs, profiles/). Here
+the same schedule is emitted as straight-line code compiled by NVRTC for sm_100a at program
+creation, so that
+
+* register-bit indices, tile layouts and global/shared offsets are compile-time constants;
+* permutation groups (CNOT, SWAP, X chains) become pure register renames (zero
+  instructions);
+* parameter-free groups (SX, ECR, MS(0,0,1/4), H, ...) use immediate matrix entries, so
+  structural zeros cost nothing;
+* a diagonal run accumulates fixed-point phases with compile-time index selection.
+
+The emitted kernels keep the generic kernel's contract (PassArgs, modes, flags, partial
+buffers), so the C ABI drivers and the emulator semantics are unchanged.
+"""
+
+from __future__ import annotations
+
+import os
+
+import numpy as np
+
+from . import schedule as S
+from .gates import GATE_TRAITS
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+PRIMS = os.path.join(_HERE, "csrc", "lsq_prims.cuh")
+
+MODE_FWD, MODE_TURN, MODE_BWD = 0, 1, 2
+
+
+def kernel_name(pi: int, mode: int) -> str:
+    return f"lsq_jit_p{pi}_m{mode}"
+
+
+def _f(x: float) -> str:
+    return repr(float(np.float32(x))) + "f"
+
+
+def _cexpr(coefs, xs):
+    """Real/imag expressions of sum_c coefs[c] * xs[c] with constant complex coefs;
+    zero terms dropped, +-1 folded."""
+    re_terms, im_terms = [], []
+    for cf, x in zip(coefs, xs):
+        a, b = float(np.real(cf)), float(np.imag(cf))
+        if abs(a) > 1e-15:
+            re_terms.append(_term(a, f"{x}.x"))
+            im_terms.append(_term(a, f"{x}.y"))
+        if abs(b) > 1e-15:
+            re_terms.append(_term(-b, f"{x}.y"))
+            im_terms.append(_term(b, f"{x}.x"))
+    return _sum(re_terms), _sum(im_terms)
+
+
+def _term(c, v):
+    if abs(c - 1.0) < 1e-15:
+        return ("+", v)
+    if abs(c + 1.0) < 1e-15:
+        return ("-", v)
+    return ("+", f"{_f(c)}*{v}")
+
+
+def _sum(terms):
+    if not terms:
+        return "0.f"
+    out = ""
+    for i, (sg, t) in enumerate(terms):
+        if i == 0:
+            out = t if sg == "+" else f"-{t}"
+        else:
+            out += f" {sg} {t}"
+    return out
+
+
+class _Pass:
+    """Compile-time view of one pass for code emission."""
+
+    def __init__(self, prog, pi):
+        self.prog = prog
+        self.pi = pi
+        self.pp = prog.passes[pi]
+        self.M = self.pp.M
+        self.R = self.pp.R
+        self.NT = 1 << (self.M - self.R)
+        self.NR = 1 << self.R
+        self.NW = (self.NT + 31) // 32
+        self.n = prog.n
+        self.pbit = list(self.pp.phys_of_local)
+        self.nbit = [p for p in range(self.n) if p not in set(self.pbit)]
+        self.enc = prog.enc[pi]
+
+    def goff(self, ph, i):
+        regs = self.pp.phases[ph].regs
+        return sum(1 << self.pbit[regs[k]] for k in range(self.R) if (i >> k) & 1)
+
+    def soff(self, ph, i):
+        regs = self.pp.phases[ph].regs
+        loc = sum(1 << regs[k] for k in range(self.R) if (i >> k) & 1)
+        return S_swz(loc)
+
+
+def S_swz(L: int) -> int:
+    h = 0
+    for j, v in enumerate(S.SWZ_H):
+        if (L >> (4 + j)) & 1:
+            h ^= v
+    return L ^ h
+
+
+# ----------------------------------------------------------------------------------------- emit
+
+
+class _W:
+    def __init__(self):
+        self.lines = []
+        self.ind = 1
+
+    def __call__(self, s=""):
+        self.lines.append("  " * self.ind + s if s else "")
+
+    def block(self, head):
+        self(head + " {")
+        self.ind += 1
+
+    def end(self, tail=""):
+        self.ind -= 1
+        self("}" + tail)
+
+
+def _group_const_matrix(grp):
+    """Compile-time matrix of a group whose parameters are all FIXED (or absent)."""
+    if any(s != S.FIXED_SRC for g, _ in grp.gates for s in g.src):
+        return None
+    return S.group_matrix_host(grp)
+
+
+def _emit_const_u(w, P, v, U, regs_bits, dagger):
+    """Constant-matrix group on register bits (list of reg indices, first = MSB)."""
+    if dagger:
+        U = np.conj(U.T)
+    d = U.shape[0]
+    R = P.R
+    if d == 2:
+        (k,) = regs_bits
+        for i in range(1 << R):
+            if (i >> k) & 1:
+                continue
+            q = [i, i | (1 << k)]
+            _emit_small(w, v, U, q)
+    else:
+        ka, kb = regs_bits
+        for i in range(1 << R):
+            if ((i >> ka) & 1) or ((i >> kb) & 1):
+                continue
+            q = [i, i | (1 << kb), i | (1 << ka), i | (1 << ka) | (1 << kb)]
+            _emit_small(w, v, U, q)
+
+
+def _emit_small(w, v, U, q):
+    """Constant complex matrix on packed f32x2: per nonzero coefficient at most two FFMA2
+    (real part times x, imaginary part times i*x); zero halves are skipped."""
+    d = len(q)
+    w("{ " + " ".join(f"const float2 x{c} = {v}[{q[c]}];" for c in range(d)))
+    for r in range(d):
+        expr = None
+        for c in range(d):
+            a, b = float(np.real(U[r, c])), float(np.imag(U[r, c]))
+            for coef, arg in ((a, f"x{c}"), (b, f"jx(x{c})")):
+                if abs(coef) < 1e-15:
+                    continue
+                if expr is None:
+                    expr = f"f2mul({arg}, bc({_f(coef)}))"
+                else:
+                    expr = f"f2fma({arg}, bc({_f(coef)}), {expr})"
+        w(f"  {v}[{q[r]}] = {expr if expr else 'make_float2(0.f, 0.f)'};")
+    w("}")
+
+
+def _src_expr(sw, P, tp_var):
+    """(kind, expr) of a diagonal source: ('reg', k) or ('const', c-expression)."""
+    kind, val = int(sw) >> 8, int(sw) & 0xFF
+    if kind == S.SRC_REG:
+        return "reg", val
+    if kind == S.SRC_THREAD:
+        return "const", f"(({tp_var} >> {val}) & 1u)"
+    if kind == S.SRC_NONLOCAL:
+        return "const", f"(int)((tbase >> {val}) & 1ull)"
+    return "none", None
+
+
+def _emit_drun(w, P, op, ph_idx, mode_bwd, nv):
+    subs = P.enc["subs"][op[6] : op[6] + op[7]]
+    tp = f"tp{ph_idx}"
+    R = P.R
+    # couplings (backward, before un-applying: conj(l) p is phase invariant)
+    if mode_bwd and any(int(s[4]) >= 0 for s in subs):
+        w("{")
+        w.ind += 1
+        for i in range(P.NR):
+            w(f"const float2 c{i} = cjmul(v[1][{i}], v[0][{i}]);")
+        for s in subs:
+            slot = int(s[4])
+            if slot < 0:
+                continue
+            ka, ea = _src_expr(s[0], P, tp)
+            kb, eb = _src_expr(s[1], P, tp)
+            ar = int(s[5])
+            # index of register i: (A bit, B bit) -> e
+            terms = {}
+            for i in range(P.NR):
+                if ar == 1:
+                    if ka == "reg":
+                        e = (i >> ea) & 1
+                    else:
+                        e = None
+                else:
+                    a = ((i >> ea) & 1) if ka == "reg" else None
+                    b = ((i >> eb) & 1) if kb == "reg" else None
+                    e = (a, b)
+                terms.setdefault(e, []).append(i)
+            w("{")
+            w.ind += 1
+            w("float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};")
+            for e, idxs in terms.items():
+                sx = " + ".join(f"c{i}.x" for i in idxs)
+                sy = " + ".join(f"c{i}.y" for i in idxs)
+                if ar == 1:
+                    ix = str(e) if e is not None else ea
+                else:
+                    if e[0] is not None and e[1] is not None:
+                        ix = str(2 * e[0] + e[1])
+                    else:
+                        a_e = str(e[0]) if e[0] is not None else ea
+                        b_e = str(e[1]) if e[1] is not None else eb
+                        ix = f"(2 * ({a_e}) + ({b_e}))"
+                if ix.isdigit():
+                    w(f"acc[{2 * int(ix)}] += {sx}; acc[{2 * int(ix) + 1}] += {sy};")
+                else:
+                    w(f"{{ const int e_ = {ix}; const float sx_ = {sx}, sy_ = {sy};")
+                    for ee in range(1 << ar):
+                        w(f"  acc[{2 * ee}] += e_ == {ee} ? sx_ : 0.f; acc[{2 * ee + 1}] += e_ == {ee} ? sy_ : 0.f;")
+                    w("}")
+            w(f"warp_accumulate8<{P.NT}>(acc, wacc + {slot});")
+            w.ind -= 1
+            w("}")
+        w.ind -= 1
+        w("}")
+    # phases
+    w("{")
+    w.ind += 1
+    w("int32_t cph = 0;")
+    per_i = [[] for _ in range(P.NR)]
+    for si, s in enumerate(subs):
+        moff = int(s[3])
+        ar = int(s[5])
+        ka, ea = _src_expr(s[0], P, tp)
+        kb, eb = _src_expr(s[1], P, tp)
+        w(f"const int32_t* a{si} = reinterpret_cast<const int32_t*>(s_mat + {moff});")
+        if ar == 1:
+            if ka == "reg":
+                for i in range(P.NR):
+                    per_i[i].append(f"a{si}[{(i >> ea) & 1}]")
+            else:
+                w(f"cph += a{si}[{ea}];")
+        else:
+            if ka != "reg" and kb != "reg":
+                w(f"cph += a{si}[2 * {ea} + {eb}];")
+            elif ka == "reg" and kb == "reg":
+                for i in range(P.NR):
+                    per_i[i].append(f"a{si}[{2 * ((i >> ea) & 1) + ((i >> eb) & 1)}]")
+            elif ka == "reg":
+                w(f"const int32_t lo{si} = a{si}[{eb}], hi{si} = a{si}[2 + {eb}];")
+                for i in range(P.NR):
+                    per_i[i].append(f"{'hi' if (i >> ea) & 1 else 'lo'}{si}")
+            else:
+                w(f"const int32_t lo{si} = a{si}[2 * {ea}], hi{si} = a{si}[2 * {ea} + 1];")
+                for i in range(P.NR):
+                    per_i[i].append(f"{'hi' if (i >> eb) & 1 else 'lo'}{si}")
+    inv = "true" if mode_bwd else "false"
+    for i in range(P.NR):
+        expr = " + ".join(["cph"] + per_i[i])
+        w(f"{{ const int32_t p_ = {expr};")
+        for q in range(nv):
+            w(f"  v[{q}][{i}] = phase_rot(v[{q}][{i}], p_, {inv});")
+        w("}")
+    w.ind -= 1
+    w("}")
+
+
+def _emit_ops(w, P, ph_idx, mode_bwd, nv):
+    ops = P.enc["ops"][ph_idx]
+    seq = list(reversed(ops)) if mode_bwd else ops
+    regs = P.pp.phases[ph_idx].regs
+    for op in seq:
+        kind = int(op[0])
+        if kind == S.OP_PX:
+            for q in range(nv):
+                w(f"perm_x<{P.R}, {int(op[1])}>(v[{q}]);")
+        elif kind == S.OP_PCX:
+            for q in range(nv):
+                w(f"perm_cx<{P.R}, {int(op[1])}, {int(op[2])}>(v[{q}]);")
+        elif kind in (S.OP_U1, S.OP_U2):
+            gid = int(op[3])
+            grp = P.prog.groups[gid]
+            bits = [int(op[1])] + ([int(op[2])] if kind == S.OP_U2 else [])
+            slot, moff = int(op[4]), int(op[5])
+            if mode_bwd and slot >= 0:
+                if kind == S.OP_U1:
+                    w(f"{{ float acc[8] = {{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}}; "
+                      f"u1_coupling<{P.R}, {bits[0]}>(v[0], v[1], acc); warp_accumulate8<{P.NT}>(acc, wacc + {slot}); }}")
+                else:
+                    for rr in range(4):
+                        w(f"{{ float acc[8] = {{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}}; "
+                          f"u2_coupling_row<{P.R}, {bits[0]}, {bits[1]}, {rr}>(v[0], v[1], acc); "
+                          f"warp_accumulate8<{P.NT}>(acc, wacc + {slot + 8 * rr}); }}")
+            U = _group_const_matrix(grp)
+            if U is not None:
+                for q in range(nv):
+                    _emit_const_u(w, P, f"v[{q}]", U, bits, mode_bwd)
+            elif kind == S.OP_U1:
+                if mode_bwd:
+                    w(f"{{ const float* g = s_mat + {moff};")
+                    for q in range(nv):
+                        w(f"  u1_apply_dag<{P.R}, {bits[0]}>(v[{q}], g);")
+                    w("}")
+                else:
+                    w(f"{{ float m[8]; for (int e = 0; e < 8; ++e) m[e] = s_mat[{moff} + e]; "
+                      f"u1_apply<{P.R}, {bits[0]}>(v[0], m); }}")
+            else:
+                if mode_bwd:
+                    for q in range(nv):
+                        w(f"u2_apply_dag<{P.R}, {bits[0]}, {bits[1]}>(v[{q}], s_mat + {moff});")
+                else:
+                    w(f"u2_apply<{P.R}, {bits[0]}, {bits[1]}>(v[0], s_mat + {moff});")
+        else:
+            _emit_drun(w, P, op, ph_idx, mode_bwd, nv)
+
+
+def _emit_exchange(w, P, a, b, nv):
+    for q in range(nv):
+        w("__syncthreads();")
+        for i in range(P.NR):
+            w(f"s_x[sx{a} ^ {P.soff(a, i)}u] = v[{q}][{i}];")
+        w("__syncthreads();")
+        for i in range(P.NR):
+            w(f"v[{q}][{i}] = s_x[sx{b} ^ {P.soff(b, i)}u];")
+
+
+def emit_kernel(prog, pi: int, mode: int) -> str:
+    P = _Pass(prog, pi)
+    nv = 1 if mode == MODE_FWD else 2
+    nph = len(P.pp.phases)
+    est_regs = 2 * P.NR * nv + 40
+    minb = max(1, min(4, 65536 // (P.NT * est_regs)))
+    matf = P.enc["matf"]
+    slotf = P.enc["slotf"]
+    w = _W()
+    out = [f'extern "C" __global__ void __launch_bounds__({P.NT}, {minb}) {kernel_name(pi, mode)}(lsq::PassArgs A) {{']
+    w("using namespace lsq;")
+    w(f"constexpr int NT = {P.NT}, NW = {P.NW}, M = {P.M};")
+    w("extern __shared__ __align__(16) unsigned char smem_raw[];")
+    w("float2* s_x = reinterpret_cast<float2*>(smem_raw);")
+    w(f"float* s_mat = reinterpret_cast<float*>(s_x + {1 << P.M});")
+    w(f"float* s_acc = s_mat + {(matf + 3) & ~3};")
+    w(f"double* s_z = reinterpret_cast<double*>(s_acc + {(P.NW * slotf + 3) & ~3});")
+    w("float* s_red = reinterpret_cast<float*>(s_z + 34);")
+    w("const int tid = threadIdx.x, warp = tid >> 5;")
+    w("const int row = blockIdx.x / A.ctas_per_row, cslot = blockIdx.x % A.ctas_per_row;")
+    w("const int mode = A.mode, flags = A.flags;")
+    w("(void)mode; (void)warp; (void)s_red;")
+    # stage group tables
+    pgs = P.enc["pgroups"]  # list of (gid, moff)
+    w("{")
+    w.ind += 1
+    for j, (gid, moff) in enumerate(pgs):
+        grp = prog.groups[gid]
+        if not grp.diag and (_group_const_matrix(grp) is not None or grp.perm_ops is not None):
+            continue  # compile-time constants, never read from the table
+        if grp.perrow:
+            ri = prog.rowidx[gid]
+            w(f"for (int e = tid; e < {grp.mat_floats}; e += NT) s_mat[{moff} + e] = A.rowtab[((size_t)row * A.nperrow + {ri}) * 32 + e];")
+        else:
+            w(f"for (int e = tid; e < {grp.mat_floats}; e += NT) s_mat[{moff} + e] = A.gmats[{gid * 32} + e];")
+    w(f"for (int i = tid; i < {P.NW * slotf}; i += NT) s_acc[i] = 0.f;")
+    w("for (int i = tid; i < 34; i += NT) s_z[i] = 0.0;")
+    w.ind -= 1
+    w("}")
+    w("__syncthreads();")
+    w(f"float* wacc = s_acc + warp * {slotf};")
+    w("(void)wacc;")
+    # per-phase thread layout constants
+    for k, ph in enumerate(P.pp.phases):
+        tp_terms = [f"(((uint32_t)tid >> {j}) & 1u) << {lb}" for j, lb in enumerate(ph.threads)]
+        gt_terms = [f"(((uint32_t)tid >> {j}) & 1u) << {P.pbit[lb]}" for j, lb in enumerate(ph.threads)]
+        w(f"const uint32_t tp{k} = {' | '.join(tp_terms) if tp_terms else '0u'};")
+        w(f"const uint32_t gt{k} = {' | '.join(gt_terms) if gt_terms else '0u'};")
+        w(f"const uint32_t st{k} = swz(tp{k});")
+        w(f"(void)tp{k}; (void)gt{k}; (void)st{k};")
+    w(f"const size_t rowbase = (size_t)row << {P.n};")
+    w("const int t0 = cslot * A.tiles_per_cta;")
+    w.block("for (int t = t0; t < t0 + A.tiles_per_cta; ++t)")
+    tb = [f"((uint64_t)((t >> {j}) & 1)) << {p}" for j, p in enumerate(P.nbit)]
+    w(f"const uint64_t tbase = {' | '.join(tb) if tb else '0ull'};")
+    # opaque per-tile copies of the shared-memory thread offsets: keeps the 2^R swizzled
+    # exchange addresses as one LOP3 each instead of hoisted (and spilled) registers
+    for k in range(nph):
+        w(f"uint32_t sx{k} = st{k}; asm volatile(\"\" : \"+r\"(sx{k}));")
+    w("const size_t base = rowbase + tbase;")
+    w(f"float2 v[{nv}][{P.NR}];")
+    last = nph - 1
+    nofwd = mode == MODE_BWD
+    if mode == MODE_TURN:
+        w("const bool nofwd = (flags & PF_NOFWD) != 0;")
+    first_expr = {MODE_FWD: "0", MODE_BWD: str(last)}.get(mode)
+
+    def emit_load(k, synth_ok):
+        if synth_ok:
+            w.block("if (flags & PF_SYNTH)")
+            for i in range(P.NR):
+                w(f"v[0][{i}] = make_float2(((tbase | (uint64_t)(gt{k} | {P.goff(k, i)}u)) == 0) ? 1.f : 0.f, 0.f);")
+            w.end()
+            w.block("else")
+        for i in range(P.NR):
+            w(f"v[0][{i}] = __ldcs(A.psi_in + base + (gt{k} | {P.goff(k, i)}u));")
+        if synth_ok:
+            w.end()
+
+    def emit_fwd_phases():
+        for k in range(nph):
+            _emit_ops(w, P, k, False, nv)
+            if k < last:
+                _emit_exchange(w, P, k, k + 1, nv)
+
+    def emit_zpart(k):
+        ph = P.pp.phases[k]
+        w("{")
+        w.ind += 1
+        w(f"float pz[{P.M + 1}];")
+        w(f"for (int e = 0; e <= {P.M}; ++e) pz[e] = 0.f;")
+        w("float S_ = 0.f;")
+        for kk in range(P.R):
+            w(f"float D{kk} = 0.f;")
+        for i in range(P.NR):
+            w(f"{{ const float pr = v[0][{i}].x * v[0][{i}].x + v[0][{i}].y * v[0][{i}].y; S_ += pr;")
+            w("  " + " ".join(f"D{kk} {'-' if (i >> kk) & 1 else '+'}= pr;" for kk in range(P.R)) + " }")
+        w(f"pz[{P.M}] = S_;")
+        for kk in range(P.R):
+            w(f"pz[{ph.regs[kk]}] += D{kk};")
+        for j, lb in enumerate(ph.threads):
+            w(f"pz[{lb}] += ((tp{k} >> {lb}) & 1u) ? -S_ : S_;")
+        w(f"warp_sum<NT, {P.M + 1}>(pz);")
+        w(f"if ((tid & 31) == 0) {{ for (int e = 0; e <= {P.M}; ++e) s_red[warp * {P.M + 1} + e] = pz[e]; }}")
+        w("__syncthreads();")
+        w.block("if (tid == 0)")
+        w(f"double tot[{P.M + 1}];")
+        w(f"for (int e = 0; e <= {P.M}; ++e) {{ double s = 0.0; for (int ww = 0; ww < NW; ++ww) s += (double)s_red[ww * {P.M + 1} + e]; tot[e] = s; }}")
+        for e, p in enumerate(P.pbit):
+            w(f"s_z[{p}] += tot[{e}];")
+        for p in P.nbit:
+            w(f"s_z[{p}] += ((tbase >> {p}) & 1ull) ? -tot[{P.M}] : tot[{P.M}];")
+        w(f"s_z[{P.n}] += tot[{P.M}];")
+        w.end()
+        w("__syncthreads();")
+        w.ind -= 1
+        w("}")
+
+    def emit_lambda_init(k):
+        ph = P.pp.phases[k]
+        w("{")
+        w.ind += 1
+        wt = lambda p: f"(A.wts ? (float)A.wts[{P.n - 1 - p}] : 1.f)"  # noqa: E731
+        terms = []
+        for lb in ph.threads:
+            p = P.pbit[lb]
+            terms.append(f"(((tp{k} >> {lb}) & 1u) ? -{wt(p)} : {wt(p)})")
+        for p in P.nbit:
+            terms.append(f"(((tbase >> {p}) & 1ull) ? -{wt(p)} : {wt(p)})")
+        w(f"const float ob = {' + '.join(terms) if terms else '0.f'};")
+        for kk in range(P.R):
+            w(f"const float w{kk} = {wt(P.pbit[ph.regs[kk]])};")
+        for i in range(P.NR):
+            o = " ".join(f"{'-' if (i >> kk) & 1 else '+'} w{kk}" for kk in range(P.R))
+            w(f"{{ const float o = ob {o}; v[1][{i}] = make_float2(o * v[0][{i}].x, o * v[0][{i}].y); }}")
+        w.ind -= 1
+        w("}")
+
+    def emit_bwd_phases():
+        for k in range(last, -1, -1):
+            _emit_ops(w, P, k, True, nv)
+            if k > 0:
+                _emit_exchange(w, P, k, k - 1, nv)
+
+    def emit_store(k, what):
+        if what == "psi":
+            w.block("if (flags & PF_STORE_PSI)")
+            for i in range(P.NR):
+                w(f"__stcs(A.psi_out + base + (gt{k} | {P.goff(k, i)}u), v[0][{i}]);")
+            w.end()
+        else:
+            w.block("if (flags & PF_STORE_LAM)")
+            for i in range(P.NR):
+                w(f"__stcs(A.lam + base + (gt{k} | {P.goff(k, i)}u), v[1][{i}]);")
+            w.end()
+
+    if mode == MODE_FWD:
+        emit_load(0, True)
+        emit_fwd_phases()
+        w.block("if (flags & PF_ZPART)")
+        emit_zpart(last)
+        w.end()
+        emit_store(last, "psi")
+    elif mode == MODE_BWD:
+        emit_load(last, False)
+        for i in range(P.NR):
+            w(f"v[1][{i}] = __ldcs(A.lam + base + (gt{last} | {P.goff(last, i)}u));")
+        emit_bwd_phases()
+        emit_store(0, "psi")
+        emit_store(0, "lam")
+    else:
+        # turnaround: forward phases (unless NOFWD), <Z>, lambda = O psi, adjoint phases
+        w.block("if (nofwd)")
+        for i in range(P.NR):
+            w(f"v[0][{i}] = __ldcs(A.psi_in + base + (gt{last} | {P.goff(last, i)}u));")
+        w.end()
+        w.block("else")
+        emit_load(0, True)
+        emit_fwd_phases()
+        w.end()
+        emit_zpart(last)
+        emit_lambda_init(last)
+        emit_bwd_phases()
+        emit_store(0, "psi")
+        emit_store(0, "lam")
+    w.end()  # tile loop
+    # flush partials
+    w("__syncthreads();")
+    if slotf:
+        w.block("if (A.part)")
+        w(f"double* dst = A.part + (size_t)blockIdx.x * {slotf};")
+        w(f"for (int f = tid; f < {slotf}; f += NT) {{ double s = 0.0; for (int ww = 0; ww < NW; ++ww) s += (double)s_acc[ww * {slotf} + f]; dst[f] = s; }}")
+        w.end()
+    w.block(f"if ((mode == PMODE_TURN || (flags & PF_ZPART)) && A.zpart)")
+    w(f"double* dst = A.zpart + (size_t)blockIdx.x * {P.n + 1};")
+    w(f"for (int f = tid; f <= {P.n}; f += NT) dst[f] = s_z[f];")
+    w.end()
+    out.extend(w.lines)
+    out.append("}")
+    return "\n".join(out)
+
+
+def program_modes(prog):
+    """(pass, mode) kernels a program needs for forward-only and forward+adjoint calls."""
+    L = len(prog.passes)
+    need = []
+    for pi in range(L):
+        need.append((pi, MODE_FWD))
+        if pi < L - 1:
+            need.append((pi, MODE_BWD))
+    need.append((L - 1, MODE_TURN))
+    return need
+
+
+def generate_kernels(prog) -> list:
+    """[(pass, mode, name, full NVRTC source)] -- one translation unit per kernel so the
+    C side can compile them in parallel."""
+    with open(PRIMS) as f:
+        prims = f.read()
+    out = []
+    for pi, mode in program_modes(prog):
+        out.append((pi, mode, kernel_name(pi, mode), prims + "\n" + emit_kernel(prog, pi, mode) + "\n"))
+    return out
+
+
+def generate(prog) -> tuple[str, list]:
+    """Full NVRTC source (primitives + kernels) and the (pass, mode, name) list."""
+    with open(PRIMS) as f:
+        prims = f.read()
+    parts = [prims, ""]
+    names = []
+    for pi, mode in program_modes(prog):
+        parts.append(emit_kernel(prog, pi, mode))
+        parts.append("")
+        names.append((pi, mode, kernel_name(pi, mode)))
+    return "\n".join(parts), names

@@ -2,6 +2,7 @@
 // forward / forward+adjoint drivers, and the small auxiliary kernels (group tables,
 // deterministic fp64 reductions, coupling contraction).
 #include <cuda_runtime.h>
+#include <nvrtc.h>
 
 #include <algorithm>
 #include <cstdio>
@@ -9,6 +10,11 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <thread>
+#include <atomic>
+#include <fstream>
+#include <sstream>
+#include <functional>
 #include <vector>
 
 #include "../../include/layersim_cuda.h"
@@ -42,6 +48,22 @@ __global__ void k_group_table(const int* W, const double* fvals, const double* t
     const int* grp = W + sec_off(W, SEC_GROUPS) + g * GROUP_WORDS;
     if (grp[GW_PERROW]) continue;
     group_table_entry(W, g, fvals, theta, nullptr, gmats + (size_t)g * 32);
+  }
+}
+
+// per-row (encoding) group tables: [row][nperrow][32]
+__global__ void k_row_table(const int* W, const double* fvals, const double* theta, const double* x,
+                            int x_stride, int batch, float* rowtab) {
+  const int ng = sec_cnt(W, SEC_GROUPS);
+  const int npr = W[HDR_NPERROW];
+  const int64_t total = (int64_t)batch * ng;
+  for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total;
+       id += (int64_t)gridDim.x * blockDim.x) {
+    const int b = (int)(id / ng), g = (int)(id % ng);
+    const int* grp = W + sec_off(W, SEC_GROUPS) + g * GROUP_WORDS;
+    if (!grp[GW_PERROW]) continue;
+    group_table_entry(W, g, fvals, theta, x + (size_t)b * x_stride,
+                      rowtab + ((size_t)b * npr + grp[GW_ROWIDX]) * 32);
   }
 }
 
@@ -188,8 +210,16 @@ struct PassInfo {
   KEntry k1, k2;
 };
 
+struct JitKernel {
+  const void* fn = nullptr;  // cudaKernel_t usable as a function handle
+  int NT = 0;
+  size_t smem_set = 0;
+};
+
 struct lsq_program {
-  int n, T, E, npasses, ngroups, slot_total;
+  std::vector<JitKernel> jit;  // [pass * 3 + mode], fn == nullptr -> generic kernel
+  std::vector<cudaLibrary_t> jit_libs;
+  int n, T, E, npasses, ngroups, slot_total, nperrow;
   int* d_words = nullptr;
   double* d_fvals = nullptr;
   std::vector<int> words;
@@ -205,8 +235,9 @@ struct lsq_program {
 namespace {
 
 size_t smem_bytes(const lsq_program* P, const PassInfo& pi, int NV) {
-  const KEntry& k = NV == 1 ? pi.k1 : pi.k2;
-  const int NW = (k.NT + 31) / 32;
+  (void)NV;
+  const int NT = 1 << (pi.M - pi.R);
+  const int NW = (NT + 31) / 32;
   size_t b = sizeof(float2) * ((size_t)1 << pi.M);
   b += sizeof(int) * ((size_t)pi.nph * PHASE_WORDS + (size_t)pi.nops * OP_WORDS + (size_t)pi.nsubs * SUB_WORDS + 64);
   b += sizeof(float) * (((pi.matf + 3) & ~3) + ((NW * pi.slotf + 3) & ~3));
@@ -237,7 +268,7 @@ struct Geometry {
 Geometry geometry(const lsq_program* P, const PassInfo& pi, int batch) {
   const int ntiles = 1 << (P->n - pi.M);
   const int64_t total = (int64_t)batch * ntiles;
-  const int64_t target = (int64_t)P->sm_count * 8;
+  const int64_t target = (int64_t)P->sm_count * 4;
   int tpc = total > target ? pow2floor(total / target) : 1;
   if (tpc > ntiles) tpc = ntiles;
   if (tpc > 64) tpc = 64;
@@ -246,6 +277,7 @@ Geometry geometry(const lsq_program* P, const PassInfo& pi, int batch) {
 
 struct WS {
   float* gmats;
+  float* rowtab;
   double* part;
   double* zpart;
   double* macc;
@@ -269,6 +301,7 @@ WS carve(const lsq_program* P, int batch, void* base) {
     maxz = std::max(maxz, (size_t)batch * g.cpr * (P->n + 1));
   }
   size_t o_g = take(sizeof(float) * 32 * (size_t)std::max(P->ngroups, 1));
+  size_t o_r = take(sizeof(float) * 32 * (size_t)batch * std::max(P->nperrow, 1));
   size_t o_p = take(sizeof(double) * std::max(maxpart, (size_t)1));
   size_t o_z = take(sizeof(double) * std::max(maxz, (size_t)1));
   size_t o_m = take(sizeof(double) * (size_t)batch * std::max(P->slot_total, 1));
@@ -278,6 +311,7 @@ WS carve(const lsq_program* P, int batch, void* base) {
   if (base) {
     char* c = (char*)base;
     w.gmats = (float*)(c + o_g);
+    w.rowtab = (float*)(c + o_r);
     w.part = (double*)(c + o_p);
     w.zpart = (double*)(c + o_z);
     w.macc = (double*)(c + o_m);
@@ -293,7 +327,10 @@ int launch_pass(lsq_program* P, int pi_idx, int mode, int flags, int batch, cons
   const PassInfo& pi = P->passes[pi_idx];
   const int NV = mode == MODE_FWD ? 1 : 2;
   const KEntry& k = NV == 1 ? pi.k1 : pi.k2;
-  if (!k.fn) return fail(LSQ_EPLAN, "no kernel instantiated for this tile size");
+  const bool have_jit = !P->jit.empty() && P->jit[pi_idx * 3 + mode].fn;
+  if (!k.fn && !have_jit)
+    return fail(LSQ_EPLAN, "no kernel for pass " + std::to_string(pi_idx) + " (M=" + std::to_string(pi.M) +
+                               ", R=" + std::to_string(pi.R) + "): attach the specialised kernels");
   Geometry g = geometry(P, pi, batch);
   PassArgs A{};
   A.prog = P->d_words;
@@ -308,6 +345,8 @@ int launch_pass(lsq_program* P, int pi_idx, int mode, int flags, int batch, cons
   A.tiles_per_cta = g.tpc;
   A.ctas_per_row = g.cpr;
   A.gmats = ws.gmats;
+  A.rowtab = ws.rowtab;
+  A.nperrow = P->nperrow;
   A.theta = theta;
   A.x = x;
   A.x_stride = x_stride;
@@ -315,6 +354,8 @@ int launch_pass(lsq_program* P, int pi_idx, int mode, int flags, int batch, cons
   A.part = ws.part;
   A.zpart = ws.zpart;
   const size_t sm = smem_bytes(P, pi, NV);
+  const JitKernel* jk = nullptr;
+  if (!P->jit.empty() && P->jit[pi_idx * 3 + mode].fn) jk = &P->jit[pi_idx * 3 + mode];
   if (P->profiling) {
     while ((int)P->ev.size() < 2 * (P->ev_used + 1)) {
       cudaEvent_t e;
@@ -323,8 +364,13 @@ int launch_pass(lsq_program* P, int pi_idx, int mode, int flags, int batch, cons
     }
     CUDA_TRY(cudaEventRecord(P->ev[2 * P->ev_used], st));
   }
-  k.fn<<<(unsigned)((int64_t)batch * g.cpr), k.NT, sm, st>>>(A);
-  CUDA_TRY(cudaGetLastError());
+  if (jk) {
+    void* args[] = {&A};
+    CUDA_TRY(cudaLaunchKernel(jk->fn, dim3((unsigned)((int64_t)batch * g.cpr)), dim3(jk->NT), args, sm, st));
+  } else {
+    k.fn<<<(unsigned)((int64_t)batch * g.cpr), k.NT, sm, st>>>(A);
+    CUDA_TRY(cudaGetLastError());
+  }
   P->launches++;
   if (P->profiling) {
     CUDA_TRY(cudaEventRecord(P->ev[2 * P->ev_used + 1], st));
@@ -402,6 +448,7 @@ int lsq_program_create(const int32_t* words, int64_t n_words, const double* fval
   P->slot_total = W[5];
   P->npasses = W[6];
   P->ngroups = W[7];
+  P->nperrow = W[HDR_NPERROW];
   if (P->n < 1 || P->n > 30) {
     delete P;
     return fail(LSQ_EINVAL, "n out of range (1..30)");
@@ -428,11 +475,10 @@ int lsq_program_create(const int32_t* words, int64_t n_words, const double* fval
     pi.first_slot = pw[PW_FIRSTSLOT];
     pi.k1 = kernel_for(pi.M, 1);
     pi.k2 = kernel_for(pi.M, 2);
-    if (!pi.k1.fn || pi.k1.R != pi.R) {
-      delete P;
-      return fail(LSQ_EPLAN, "pass " + std::to_string(i) + ": no kernel for M=" + std::to_string(pi.M) +
-                                 " R=" + std::to_string(pi.R));
-    }
+    // the generic (interpreting) kernels exist for R = r_of(M) only; other register tilings
+    // run exclusively on the per-program specialised kernels (lsq_program_jit)
+    if (pi.k1.R != pi.R) pi.k1.fn = nullptr;
+    if (pi.k2.R != pi.R) pi.k2.fn = nullptr;
     P->passes.push_back(pi);
     for (int NV = 1; NV <= 2; ++NV) {
       const KEntry& k = NV == 1 ? pi.k1 : pi.k2;
@@ -457,8 +503,112 @@ int lsq_program_create(const int32_t* words, int64_t n_words, const double* fval
   return LSQ_OK;
 }
 
+namespace {
+
+uint64_t fnv1a(const char* s, size_t n) {
+  uint64_t h = 1469598103934665603ull;
+  for (size_t i = 0; i < n; ++i) {
+    h ^= (unsigned char)s[i];
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+
+bool read_file(const std::string& path, std::string& out) {
+  std::ifstream f(path, std::ios::binary);
+  if (!f) return false;
+  std::stringstream ss;
+  ss << f.rdbuf();
+  out = ss.str();
+  return !out.empty();
+}
+
+// NVRTC: source -> sm_100a cubin (with an optional on-disk cache keyed by the source hash)
+int jit_compile(const std::string& src, const std::string& cache_dir, std::string& cubin, std::string& log) {
+  std::string key;
+  if (!cache_dir.empty()) {
+    char buf[40];
+    snprintf(buf, sizeof buf, "%016llx", (unsigned long long)fnv1a(src.data(), src.size()));
+    key = cache_dir + "/lsq_" + buf + ".cubin";
+    if (read_file(key, cubin)) return 0;
+  }
+  nvrtcProgram prog;
+  if (nvrtcCreateProgram(&prog, src.c_str(), "lsq_jit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) {
+    log = "nvrtcCreateProgram failed";
+    return 1;
+  }
+  const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo", "-DNDEBUG"};
+  nvrtcResult rc = nvrtcCompileProgram(prog, 4, opts);
+  size_t ls = 0;
+  nvrtcGetProgramLogSize(prog, &ls);
+  if (ls > 1) {
+    log.resize(ls);
+    nvrtcGetProgramLog(prog, &log[0]);
+  }
+  if (rc != NVRTC_SUCCESS) {
+    nvrtcDestroyProgram(&prog);
+    return 1;
+  }
+  size_t cs = 0;
+  nvrtcGetCUBINSize(prog, &cs);
+  cubin.resize(cs);
+  nvrtcGetCUBIN(prog, &cubin[0]);
+  nvrtcDestroyProgram(&prog);
+  if (!key.empty()) {
+    std::string tmp = key + ".tmp" + std::to_string((unsigned long long)std::hash<std::thread::id>{}(std::this_thread::get_id()));
+    std::ofstream f(tmp, std::ios::binary);
+    if (f) {
+      f.write(cubin.data(), (std::streamsize)cubin.size());
+      f.close();
+      std::rename(tmp.c_str(), key.c_str());
+    }
+  }
+  return 0;
+}
+
+}  // namespace
+
+int lsq_program_jit(lsq_program* P, int nk, const char* const* sources, const int* pass_idx,
+                    const int* modes, const char* const* names, const char* cache_dir, int threads) {
+  if (!P || nk < 0 || (nk && (!sources || !pass_idx || !modes || !names)))
+    return fail(LSQ_EINVAL, "bad JIT arguments");
+  std::vector<std::string> cubins(nk), logs(nk);
+  std::vector<int> rcs(nk, 0);
+  std::atomic<int> next{0};
+  const std::string cdir = cache_dir ? cache_dir : "";
+  int nt = threads > 0 ? threads : (int)std::thread::hardware_concurrency();
+  nt = std::max(1, std::min(nt, nk));
+  std::vector<std::thread> pool;
+  for (int t = 0; t < nt; ++t)
+    pool.emplace_back([&]() {
+      for (int i = next++; i < nk; i = next++) rcs[i] = jit_compile(sources[i], cdir, cubins[i], logs[i]);
+    });
+  for (auto& th : pool) th.join();
+  for (int i = 0; i < nk; ++i)
+    if (rcs[i]) return fail(LSQ_EINVAL, std::string("NVRTC failed for ") + names[i] + ":\n" + logs[i].substr(0, 4000));
+  P->jit.assign((size_t)P->npasses * 3, JitKernel{});
+  for (int i = 0; i < nk; ++i) {
+    if (pass_idx[i] < 0 || pass_idx[i] >= P->npasses || modes[i] < 0 || modes[i] > 2)
+      return fail(LSQ_EINVAL, "bad JIT kernel index");
+    cudaLibrary_t lib;
+    CUDA_TRY(cudaLibraryLoadData(&lib, cubins[i].data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
+    P->jit_libs.push_back(lib);
+    cudaKernel_t kern;
+    CUDA_TRY(cudaLibraryGetKernel(&kern, lib, names[i]));
+    JitKernel& jk = P->jit[pass_idx[i] * 3 + modes[i]];
+    jk.fn = (const void*)kern;
+    const PassInfo& pi = P->passes[pass_idx[i]];
+    jk.NT = 1 << (pi.M - pi.R);
+    const size_t sm = smem_bytes(P, pi, modes[i] == 0 ? 1 : 2);
+    CUDA_TRY(cudaFuncSetAttribute(jk.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    jk.smem_set = sm;
+  }
+  return LSQ_OK;
+}
+
 void lsq_program_destroy(lsq_program* P) {
   if (!P) return;
+  for (auto l : P->jit_libs) cudaLibraryUnload(l);
   for (auto e : P->ev) cudaEventDestroy(e);
   cudaFree(P->d_words);
   cudaFree(P->d_fvals);
@@ -512,6 +662,11 @@ int lsq_forward(const lsq_program* Pc, int batch, const double* theta, const dou
   P->launches = 0;
   k_group_table<<<std::max(1, (P->ngroups + 127) / 128), 128, 0, st>>>(P->d_words, P->d_fvals, theta, ws.gmats);
   P->launches++;
+  if (P->nperrow && x) {
+    const int64_t tot = (int64_t)batch * P->ngroups;
+    k_row_table<<<(int)std::min<int64_t>((tot + 127) / 128, 8192), 128, 0, st>>>(P->d_words, P->d_fvals, theta, x, x_stride, batch, ws.rowtab);
+    P->launches++;
+  }
   CUDA_TRY(cudaGetLastError());
   const float2* src = (const float2*)psi_in;
   float2* dst = (float2*)psi_out;
@@ -551,6 +706,11 @@ int lsq_fwd_bwd(const lsq_program* Pc, int batch, const double* theta, const dou
   float2* lam = (float2*)lam_v;
   k_group_table<<<std::max(1, (P->ngroups + 127) / 128), 128, 0, st>>>(P->d_words, P->d_fvals, theta, ws.gmats);
   P->launches++;
+  if (P->nperrow && x) {
+    const int64_t tot = (int64_t)batch * P->ngroups;
+    k_row_table<<<(int)std::min<int64_t>((tot + 127) / 128, 8192), 128, 0, st>>>(P->d_words, P->d_fvals, theta, x, x_stride, batch, ws.rowtab);
+    P->launches++;
+  }
   CUDA_TRY(cudaGetLastError());
   const int64_t mtot = (int64_t)batch * std::max(P->slot_total, 1);
   k_zero<<<(int)std::min<int64_t>((mtot + 255) / 256, 4096), 256, 0, st>>>(ws.macc, mtot);
@@ -597,6 +757,11 @@ int lsq_bwd_from_state(const lsq_program* Pc, int batch, const double* theta, co
   float2* lam = (float2*)lam_v;
   k_group_table<<<std::max(1, (P->ngroups + 127) / 128), 128, 0, st>>>(P->d_words, P->d_fvals, theta, ws.gmats);
   P->launches++;
+  if (P->nperrow && x) {
+    const int64_t tot = (int64_t)batch * P->ngroups;
+    k_row_table<<<(int)std::min<int64_t>((tot + 127) / 128, 8192), 128, 0, st>>>(P->d_words, P->d_fvals, theta, x, x_stride, batch, ws.rowtab);
+    P->launches++;
+  }
   CUDA_TRY(cudaGetLastError());
   const int64_t mtot = (int64_t)batch * std::max(P->slot_total, 1);
   k_zero<<<(int)std::min<int64_t>((mtot + 255) / 256, 4096), 256, 0, st>>>(ws.macc, mtot);

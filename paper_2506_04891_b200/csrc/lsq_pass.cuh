@@ -21,6 +21,7 @@
 #include <type_traits>
 
 #include "lsq_common.cuh"
+#include "lsq_prims.cuh"
 
 namespace lsq {
 
@@ -31,34 +32,6 @@ constexpr int F_SYNTH = 1,      // input psi is |0..0> (not read)
     F_ZPART = 8,                // forward: accumulate <Z_q> partials of the output
     F_NOFWD = 16;               // turnaround on a given final state: skip the forward ops
 
-struct PassArgs {
-  const int* prog;       // device program words
-  const double* fvals;   // fixed gate parameters
-  int pass;
-  int mode, flags;
-  int n;
-  const float2* psi_in;  // row stride 2^n
-  float2* psi_out;
-  float2* lam;
-  int tiles_per_cta, ctas_per_row;
-  const float* gmats;  // shared group table, 32 floats per group
-  const double* theta;
-  const double* x;
-  int x_stride;
-  const double* wts;  // n weights (device) or null = ones
-  double* part;       // [grid][pass slot floats]
-  double* zpart;      // [grid][n+1] indexed by physical bit, [n] = norm
-};
-
-// shared-memory XOR swizzle (schedule.SWZ_H)
-__host__ __device__ __forceinline__ uint32_t swz(uint32_t L) {
-  const uint32_t H[14] = {1, 2, 4, 8, 3, 6, 12, 11, 5, 10, 7, 14, 15, 9};
-  uint32_t h = 0;
-#pragma unroll
-  for (int j = 0; j < 14; ++j)
-    if ((L >> (4 + j)) & 1u) h ^= H[j];
-  return L ^ h;
-}
 
 template <int R>
 struct Layout {
@@ -132,98 +105,6 @@ __device__ __forceinline__ void dispatch2(int a, int b, F&& f) {
     } else {
       dispatch2<R, A + 1, 0>(a, b, f);
     }
-  }
-}
-
-// ---- complex fp32 -------------------------------------------------------------------------
-__device__ __forceinline__ float2 cm(float ar, float ai, float2 x) {
-  return make_float2(ar * x.x - ai * x.y, ar * x.y + ai * x.x);
-}
-__device__ __forceinline__ float2 cfma(float ar, float ai, float2 x, float2 acc) {
-  acc.x = fmaf(ar, x.x, fmaf(-ai, x.y, acc.x));
-  acc.y = fmaf(ar, x.y, fmaf(ai, x.x, acc.y));
-  return acc;
-}
-// conj(l) * p accumulated into (re, im)
-__device__ __forceinline__ void cjacc(float2 l, float2 p, float& re, float& im) {
-  re = fmaf(l.x, p.x, fmaf(l.y, p.y, re));
-  im = fmaf(l.x, p.y, fmaf(-l.y, p.x, im));
-}
-
-// ---- 1-qubit group on register bit K ------------------------------------------------------
-template <int R, int K>
-__device__ __forceinline__ void u1_apply(float2* a, const float* m) {
-#pragma unroll
-  for (int i = 0; i < (1 << R); ++i) {
-    if ((i >> K) & 1) continue;
-    const int j = i | (1 << K);
-    float2 x0 = a[i], x1 = a[j];
-    a[i] = cfma(m[2], m[3], x1, cm(m[0], m[1], x0));
-    a[j] = cfma(m[6], m[7], x1, cm(m[4], m[5], x0));
-  }
-}
-// coupling M_ab = sum conj(l_a) p_b at the current point, 8 floats (a,b row-major)
-template <int R, int K>
-__device__ __forceinline__ void u1_coupling(const float2* p, const float2* l, float* acc) {
-#pragma unroll
-  for (int i = 0; i < (1 << R); ++i) {
-    if ((i >> K) & 1) continue;
-    const int j = i | (1 << K);
-    cjacc(l[i], p[i], acc[0], acc[1]);
-    cjacc(l[i], p[j], acc[2], acc[3]);
-    cjacc(l[j], p[i], acc[4], acc[5]);
-    cjacc(l[j], p[j], acc[6], acc[7]);
-  }
-}
-
-// ---- 2-qubit group on register bits (KA = first wire, more significant; KB) -----------------
-template <int R, int KA, int KB>
-__device__ __forceinline__ void u2_apply(float2* a, const float* m) {
-#pragma unroll
-  for (int i = 0; i < (1 << R); ++i) {
-    if (((i >> KA) & 1) || ((i >> KB) & 1)) continue;
-    const int q[4] = {i, i | (1 << KB), i | (1 << KA), i | (1 << KA) | (1 << KB)};
-    float2 x[4] = {a[q[0]], a[q[1]], a[q[2]], a[q[3]]};
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      float2 acc = cm(m[8 * r], m[8 * r + 1], x[0]);
-#pragma unroll
-      for (int c = 1; c < 4; ++c) acc = cfma(m[8 * r + 2 * c], m[8 * r + 2 * c + 1], x[c], acc);
-      a[q[r]] = acc;
-    }
-  }
-}
-template <int R, int KA, int KB>
-__device__ __forceinline__ void u2_coupling(const float2* p, const float2* l, float* acc) {
-#pragma unroll
-  for (int i = 0; i < (1 << R); ++i) {
-    if (((i >> KA) & 1) || ((i >> KB) & 1)) continue;
-    const int q[4] = {i, i | (1 << KB), i | (1 << KA), i | (1 << KA) | (1 << KB)};
-#pragma unroll
-    for (int r = 0; r < 4; ++r)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) cjacc(l[q[r]], p[q[c]], acc[8 * r + 2 * c], acc[8 * r + 2 * c + 1]);
-  }
-}
-
-// ---- reductions -----------------------------------------------------------------------------
-template <int NT, int NV>
-__device__ __forceinline__ void warp_sum(float (&v)[NV]) {
-  constexpr int WL = NT < 32 ? NT : 32;
-  constexpr unsigned MASK = WL == 32 ? 0xffffffffu : ((1u << WL) - 1u);
-#pragma unroll
-  for (int o = WL / 2; o > 0; o >>= 1)
-#pragma unroll
-    for (int e = 0; e < NV; ++e) v[e] += __shfl_xor_sync(MASK, v[e], o);
-}
-
-// add per-thread values into this warp's shared accumulator slot
-template <int NT, int NV>
-__device__ __forceinline__ void warp_accumulate(float (&v)[NV], float* dst) {
-  warp_sum<NT, NV>(v);
-  if ((threadIdx.x & 31) == 0) {
-#pragma unroll
-    for (int e = 0; e < NV; ++e) dst[e] += v[e];
   }
 }
 
@@ -314,17 +195,12 @@ __device__ __forceinline__ void apply_phases(const int32_t (&ph)[1 << R], float2
   }
 }
 
-// couplings of a diagonal run: M_e = sum conj(l) p over amplitudes with local index e
+// couplings of a diagonal run: M_e = sum conj(l) p over amplitudes with local index e.
+// conj(l) p is recomputed per sub-op (no 2^R-entry temporary -> no register spills).
+
 template <int NT, int R>
 __device__ __forceinline__ void drun_couplings(const int* subs, int nsub, const float2* p, const float2* l,
                                                uint32_t tp, uint64_t tbase, float* wacc) {
-  float2 pr[1 << R];
-#pragma unroll
-  for (int i = 0; i < (1 << R); ++i) {
-    float re = 0.f, im = 0.f;
-    cjacc(l[i], p[i], re, im);
-    pr[i] = make_float2(re, im);
-  }
   for (int s = 0; s < nsub; ++s) {
     const int* sw = subs + s * SUB_WORDS;
     const int slot = sw[4];
@@ -332,66 +208,42 @@ __device__ __forceinline__ void drun_couplings(const int* subs, int nsub, const 
     const int sa = sw[0], sb = sw[1], ar = sw[5];
     const int ka = sa >> 8, kb = sb >> 8;
     float v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    // v[2e], v[2e+1] = partial M_e ; e in [0, 2^ar)
-    if (ar == 1) {
-      if (ka == SRC_REG) {
-        float a0x = 0, a0y = 0, a1x = 0, a1y = 0;
-        dispatch1<R>(sa & 0xff, [&](auto K) {
-#pragma unroll
-          for (int i = 0; i < (1 << R); ++i) {
-            if ((i >> K.value) & 1) { a1x += pr[i].x; a1y += pr[i].y; }
-            else { a0x += pr[i].x; a0y += pr[i].y; }
-          }
-        });
-        v[0] = a0x; v[1] = a0y; v[2] = a1x; v[3] = a1y;
-      } else {
-        float tx = 0, ty = 0;
-#pragma unroll
-        for (int i = 0; i < (1 << R); ++i) { tx += pr[i].x; ty += pr[i].y; }
-        const int e = src_const_bit(sa, tp, tbase);
-        v[2 * e] = tx; v[2 * e + 1] = ty;
-      }
-    } else if (ka != SRC_REG && kb != SRC_REG) {
+    const bool ra = ka == SRC_REG, rb = (ar == 2) && kb == SRC_REG;
+    if (!ra && !rb) {
       float tx = 0, ty = 0;
 #pragma unroll
-      for (int i = 0; i < (1 << R); ++i) { tx += pr[i].x; ty += pr[i].y; }
-      const int e = 2 * src_const_bit(sa, tp, tbase) + src_const_bit(sb, tp, tbase);
-      v[2 * e] = tx; v[2 * e + 1] = ty;
-    } else if (ka == SRC_REG && kb != SRC_REG) {
-      const int bb = src_const_bit(sb, tp, tbase);
+      for (int i = 0; i < (1 << R); ++i) { const float2 c = cjmul(l[i], p[i]); tx += c.x; ty += c.y; }
+      const int e = ar == 1 ? src_const_bit(sa, tp, tbase)
+                            : 2 * src_const_bit(sa, tp, tbase) + src_const_bit(sb, tp, tbase);
+      v[2 * e] = tx;
+      v[2 * e + 1] = ty;
+    } else if (ra != rb) {
+      // one register source: split by that register bit; the other index bit is constant
+      const int k = ra ? (sa & 0xff) : (sb & 0xff);
       float a0x = 0, a0y = 0, a1x = 0, a1y = 0;
-      dispatch1<R>(sa & 0xff, [&](auto K) {
+      dispatch1<R>(k, [&](auto K) {
 #pragma unroll
         for (int i = 0; i < (1 << R); ++i) {
-          if ((i >> K.value) & 1) { a1x += pr[i].x; a1y += pr[i].y; }
-          else { a0x += pr[i].x; a0y += pr[i].y; }
+          const float2 c = cjmul(l[i], p[i]);
+          if ((i >> K.value) & 1) { a1x += c.x; a1y += c.y; }
+          else { a0x += c.x; a0y += c.y; }
         }
       });
-      v[2 * bb] = a0x; v[2 * bb + 1] = a0y; v[2 * (2 + bb)] = a1x; v[2 * (2 + bb) + 1] = a1y;
-    } else if (ka != SRC_REG && kb == SRC_REG) {
-      const int ba = src_const_bit(sa, tp, tbase);
-      float a0x = 0, a0y = 0, a1x = 0, a1y = 0;
-      dispatch1<R>(sb & 0xff, [&](auto K) {
-#pragma unroll
-        for (int i = 0; i < (1 << R); ++i) {
-          if ((i >> K.value) & 1) { a1x += pr[i].x; a1y += pr[i].y; }
-          else { a0x += pr[i].x; a0y += pr[i].y; }
-        }
-      });
-      v[2 * (2 * ba)] = a0x; v[2 * (2 * ba) + 1] = a0y; v[2 * (2 * ba + 1)] = a1x; v[2 * (2 * ba + 1) + 1] = a1y;
+      int e0, e1;
+      if (ar == 1) { e0 = 0; e1 = 1; }
+      else if (ra) { const int bb = src_const_bit(sb, tp, tbase); e0 = bb; e1 = 2 + bb; }
+      else { const int ba = src_const_bit(sa, tp, tbase); e0 = 2 * ba; e1 = 2 * ba + 1; }
+      v[2 * e0] = a0x; v[2 * e0 + 1] = a0y; v[2 * e1] = a1x; v[2 * e1 + 1] = a1y;
     } else {
-      const int a = sa & 0xff, b = sb & 0xff;
-      float q[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      dispatch2<R>(a, b, [&](auto A, auto B) {
+      dispatch2<R>(sa & 0xff, sb & 0xff, [&](auto A, auto B) {
 #pragma unroll
         for (int i = 0; i < (1 << R); ++i) {
+          const float2 c = cjmul(l[i], p[i]);
           const int e = 2 * ((i >> A.value) & 1) + ((i >> B.value) & 1);
-          q[2 * e] += pr[i].x;
-          q[2 * e + 1] += pr[i].y;
+          v[2 * e] += c.x;
+          v[2 * e + 1] += c.y;
         }
       });
-#pragma unroll
-      for (int e = 0; e < 8; ++e) v[e] = q[e];
     }
     warp_accumulate<NT, 8>(v, wacc + slot);
   }
@@ -399,7 +251,8 @@ __device__ __forceinline__ void drun_couplings(const int* subs, int nsub, const 
 
 // ---- the kernel ---------------------------------------------------------------------------------
 template <int M, int R, int NV>
-__global__ void __launch_bounds__(1 << (M - R)) lsq_pass_kernel(PassArgs A) {
+__global__ void __launch_bounds__(1 << (M - R), (NV == 1 && (1 << (M - R)) <= 256) ? 2 : 1)
+    lsq_pass_kernel(PassArgs A) {
   constexpr int NT = 1 << (M - R);
   constexpr int NR = 1 << R;
   constexpr int NW = (NT + 31) / 32;
@@ -443,21 +296,21 @@ __global__ void __launch_bounds__(1 << (M - R)) lsq_pass_kernel(PassArgs A) {
       }
     }
     const int row = blockIdx.x / A.ctas_per_row;
-    const double* xrow = A.x ? A.x + (size_t)row * A.x_stride : nullptr;
     const int* pg = W + sec_off(W, SEC_PGROUPS) + pw[PW_PG0] * PGROUP_WORDS;
     const int* groups = W + sec_off(W, SEC_GROUPS);
     for (int g = tid; g < pw[PW_NGRP]; g += NT) {
       const int gid = pg[g * PGROUP_WORDS], moff = pg[g * PGROUP_WORDS + 1];
       const int* grp = groups + gid * GROUP_WORDS;
       if (grp[GW_PERROW]) {
-        group_table_entry(W, gid, A.fvals, A.theta, xrow, s_mat + moff);
+        const float* src = A.rowtab + ((size_t)row * A.nperrow + grp[GW_ROWIDX]) * 32;
+        for (int e = 0; e < grp[GW_MATF]; ++e) s_mat[moff + e] = src[e];
       } else {
         const float* src = A.gmats + (size_t)gid * 32;
         for (int e = 0; e < grp[GW_MATF]; ++e) s_mat[moff + e] = src[e];
       }
     }
     for (int i = tid; i < NW * slotf; i += NT) s_acc[i] = 0.f;
-    if (tid < 34) s_z[tid] = 0.0;
+    for (int i = tid; i < 34; i += NT) s_z[i] = 0.0;
   }
   __syncthreads();
 
@@ -493,8 +346,14 @@ __global__ void __launch_bounds__(1 << (M - R)) lsq_pass_kernel(PassArgs A) {
 #pragma unroll
         for (int e = 0; e < 8; ++e) m[e] = s_mat[op[5] + e];
         dispatch1<R>(op[1], [&](auto K) { u1_apply<R, K.value>(v[0], m); });
+      } else if (kind == OP_PCX) {
+        dispatch2<R>(op[1], op[2], [&](auto KC, auto KT) { perm_cx<R, KC.value, KT.value>(v[0]); });
+      } else if (kind == OP_PX) {
+        dispatch1<R>(op[1], [&](auto K) { perm_x<R, K.value>(v[0]); });
       } else if (kind == OP_U2) {
-        const float* m = s_mat + op[5];
+        float m[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) m[e] = s_mat[op[5] + e];
         dispatch2<R>(op[1], op[2], [&](auto KA, auto KB) { u2_apply<R, KA.value, KB.value>(v[0], m); });
       } else {
         int32_t ph_[NR];
@@ -511,7 +370,17 @@ __global__ void __launch_bounds__(1 << (M - R)) lsq_pass_kernel(PassArgs A) {
     for (int o = o0 + no - 1; o >= o0; --o) {
       const int* op = s_ops + o * OP_WORDS;
       const int kind = op[0];
-      if (kind == OP_U1) {
+      if (kind == OP_PCX) {
+        dispatch2<R>(op[1], op[2], [&](auto KC, auto KT) {
+#pragma unroll
+          for (int q = 0; q < NV; ++q) perm_cx<R, KC.value, KT.value>(v[q]);
+        });
+      } else if (kind == OP_PX) {
+        dispatch1<R>(op[1], [&](auto K) {
+#pragma unroll
+          for (int q = 0; q < NV; ++q) perm_x<R, K.value>(v[q]);
+        });
+      } else if (kind == OP_U1) {
         const float* g = s_mat + op[5];
         if constexpr (NV == 2) {
           if (op[4] >= 0) {
@@ -530,24 +399,23 @@ __global__ void __launch_bounds__(1 << (M - R)) lsq_pass_kernel(PassArgs A) {
         const float* g = s_mat + op[5];
         if constexpr (NV == 2) {
           if (op[4] >= 0) {
-            float acc[32];
-#pragma unroll
-            for (int e = 0; e < 32; ++e) acc[e] = 0.f;
-            dispatch2<R>(op[1], op[2], [&](auto KA, auto KB) { u2_coupling<R, KA.value, KB.value>(v[0], v[1], acc); });
-            warp_accumulate<NT, 32>(acc, wacc + op[4]);
+            dispatch2<R>(op[1], op[2], [&](auto KA, auto KB) {
+              auto row = [&](auto RRc) {
+                float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                u2_coupling_row<R, KA.value, KB.value, RRc.value>(v[0], v[1], acc);
+                warp_accumulate<NT, 8>(acc, wacc + op[4] + 8 * RRc.value);
+              };
+              row(std::integral_constant<int, 0>{});
+              row(std::integral_constant<int, 1>{});
+              row(std::integral_constant<int, 2>{});
+              row(std::integral_constant<int, 3>{});
+            });
           }
         }
-        float m[32];
-#pragma unroll
-        for (int r = 0; r < 4; ++r)
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            m[8 * r + 2 * c] = g[8 * c + 2 * r];
-            m[8 * r + 2 * c + 1] = -g[8 * c + 2 * r + 1];
-          }
+        // U^dag straight from the shared table (conj transpose)
         dispatch2<R>(op[1], op[2], [&](auto KA, auto KB) {
 #pragma unroll
-          for (int q = 0; q < NV; ++q) u2_apply<R, KA.value, KB.value>(v[q], m);
+          for (int q = 0; q < NV; ++q) u2_apply_dag<R, KA.value, KB.value>(v[q], g);
         });
       } else {
         const int* subs = s_subs + (op[6] - pw[PW_SUBLO]) * SUB_WORDS;

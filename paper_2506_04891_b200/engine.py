@@ -10,6 +10,7 @@ processed in micro-batches when psi+lambda for the whole batch would not fit in 
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 import torch
@@ -57,6 +58,31 @@ class NativeProgram:
             )
         self.handle = h
         self._ws = {}
+        self.jit = False
+
+    def attach_jit(self, cache_dir=None):
+        """Compile the per-pass specialised kernels (codegen.py) with NVRTC for sm_100a."""
+        from . import codegen
+
+        ks = codegen.generate_kernels(self.prog)
+        n = len(ks)
+        srcs = (ctypes.c_char_p * n)(*[k[3].encode() for k in ks])
+        names = (ctypes.c_char_p * n)(*[k[2].encode() for k in ks])
+        pidx = (ctypes.c_int * n)(*[k[0] for k in ks])
+        modes = (ctypes.c_int * n)(*[k[1] for k in ks])
+        if cache_dir is None:
+            cache_dir = os.environ.get("LSQ_CACHE_DIR", os.path.join(os.path.expanduser("~"), ".cache", "lsq_jit"))
+        if cache_dir:
+            os.makedirs(cache_dir, exist_ok=True)
+        with torch.cuda.device(self.device):
+            _native.check(
+                _native.lib().lsq_program_jit(
+                    self.handle, n, ctypes.cast(srcs, ctypes.c_void_p), ctypes.cast(pidx, ctypes.c_void_p),
+                    ctypes.cast(modes, ctypes.c_void_p), ctypes.cast(names, ctypes.c_void_p),
+                    cache_dir.encode() if cache_dir else None, 0,
+                )
+            )
+        self.jit = True
 
     def __del__(self):
         h = getattr(self, "handle", None)
@@ -94,7 +120,7 @@ class NativeProgram:
 class Engine:
     """A circuit compiled for the device; the object behind the drop-in API."""
 
-    def __init__(self, circuit, M: int | None = None, R: int | None = None, device=None):
+    def __init__(self, circuit, M: int | None = None, R: int | None = None, device=None, jit=None):
         self.device = torch.device(device if device is not None else "cuda")
         if self.device.type != "cuda":
             raise ValueError("the engine runs on CUDA devices only")
@@ -102,6 +128,11 @@ class Engine:
         self.n = int(circuit.n)
         self.program = compile_circuit(circuit, M=M, R=R)
         self.native = NativeProgram(self.program, self.device)
+        if jit is None:
+            jit = os.environ.get("LSQ_JIT", "1") != "0"
+        if jit:
+            self.native.attach_jit()
+        self.variant = "jit" if jit else "interp"
         self.T = self.program.trainable_count
         self.E = self.program.encoding_count
 
@@ -236,15 +267,15 @@ class Engine:
 _CACHE: dict = {}
 
 
-def engine_for(circuit, device=None, M=None, R=None) -> Engine:
-    """Cached Engine per (circuit layers, n, tiling, device)."""
+def engine_for(circuit, device=None, M=None, R=None, jit=None) -> Engine:
+    """Cached Engine per (circuit layers, n, tiling, variant, device)."""
     dev = torch.device(device if device is not None else "cuda")
     if dev.type == "cuda" and dev.index is None:
         dev = torch.device("cuda", torch.cuda.current_device())
-    key = (_circuit_key(circuit), M, R, str(dev))
+    key = (_circuit_key(circuit), M, R, jit, str(dev))
     eng = _CACHE.get(key)
     if eng is None:
-        eng = Engine(circuit, M=M, R=R, device=dev)
+        eng = Engine(circuit, M=M, R=R, device=dev, jit=jit)
         _CACHE[key] = eng
     return eng
 

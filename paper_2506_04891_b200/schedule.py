@@ -45,7 +45,7 @@ ENC_FLAG = 1 << 30  # param source tag: encoding column
 FIXED_SRC = -1
 
 # op kinds (must match csrc/lsq_program.h)
-OP_U1, OP_U2, OP_DRUN = 1, 2, 3
+OP_U1, OP_U2, OP_DRUN, OP_PX, OP_PCX = 1, 2, 3, 4, 5  # PX: X on reg a; PCX: CX reg a -> reg b
 # diag source kinds
 SRC_NONE, SRC_REG, SRC_THREAD, SRC_NONLOCAL = 0, 1, 2, 3
 MAGIC = 0x4C535131  # "LSQ1"
@@ -153,12 +153,80 @@ class Group:
         return 8 if self.arity == 1 else 32
 
     @property
+    def perm_ops(self):
+        """For a parameter-free group whose unitary is a 0/1 permutation matrix: the shortest
+        sequence of register primitives ('x', bit) / ('cx', ctrl, tgt) realising it (bit 0 =
+        first group wire, the more significant local bit); None otherwise."""
+        if any(GATE_TRAITS[g.kind].param_count for g, _ in self.gates):
+            return None
+        U = group_matrix_host(self)
+        d = U.shape[0]
+        if not (np.all((np.abs(U) < 1e-12) | (np.abs(U - 1) < 1e-12)) and np.allclose(np.abs(U).sum(0), 1)):
+            return None
+        target = tuple(int(np.argmax(np.abs(U[:, c]))) for c in range(d))  # |c> -> |target[c]>
+        return _perm_sequence(target, self.arity)
+
+    @property
     def slot_floats(self) -> int:
         if not self.needs_grad:
             return 0
         if self.diag:
             return 2 << self.arity  # complex diagonal of M
         return 8 if self.arity == 1 else 32
+
+
+def group_matrix_host(grp: Group) -> np.ndarray:
+    """Unitary of a parameter-free group in its basis (host fp64)."""
+    from .gates import gate_matrix
+
+    d = 1 << grp.arity
+    U = np.eye(d, dtype=complex)
+    P = np.eye(4)[[0, 2, 1, 3]]
+    for g, rev in grp.gates:
+        G = gate_matrix(g.kind, g.fixed if g.fixed else None) if GATE_TRAITS[g.kind].param_count else gate_matrix(g.kind)
+        if rev:
+            G = P @ G @ P
+        U = G @ U
+    return U
+
+
+def _perm_sequence(target, arity):
+    """BFS over the primitives X_A, X_B, CX(A->B), CX(B->A) on local basis indices."""
+    from collections import deque
+
+    d = 1 << arity
+    if arity == 1:
+        prims = [("x", 0)]
+    else:
+        prims = [("x", 0), ("x", 1), ("cx", 0, 1), ("cx", 1, 0)]
+
+    def act(p, idx):
+        bits = [(idx >> (arity - 1 - k)) & 1 for k in range(arity)]  # bit 0 = first wire (MSB)
+        if p[0] == "x":
+            bits[p[1]] ^= 1
+        else:
+            bits[p[2]] ^= bits[p[1]]
+        return sum(b << (arity - 1 - k) for k, b in enumerate(bits))
+
+    start = tuple(range(d))
+    goal = tuple(target)
+    prev = {start: None}
+    q = deque([start])
+    while q:
+        cur = q.popleft()
+        if cur == goal:
+            break
+        for p in prims:
+            nxt = tuple(act(p, v) for v in cur)
+            if nxt not in prev:
+                prev[nxt] = (cur, p)
+                q.append(nxt)
+    seq = []
+    cur = goal
+    while prev[cur] is not None:
+        cur, p = prev[cur]
+        seq.append(p)
+    return seq[::-1]
 
 
 def fuse_groups(gates: list[GateRef]) -> list[Group]:
@@ -405,6 +473,8 @@ class Program:
     fvals: np.ndarray = None
     M: int = 0
     gates: list = None
+    enc: list = None  # per pass: ops per phase, subs, table sizes (consumed by codegen)
+    rowidx: dict = None  # gid -> per-row table index
 
     @property
     def n_passes(self) -> int:
@@ -456,6 +526,7 @@ def encode(prog: Program) -> None:
     gates_w, fvals = [], []
     group_w = []
     gate_index = 0
+    rowidx = 0
     for g in prog.groups:
         g0 = gate_index
         for gate, rev in g.gates:
@@ -470,9 +541,17 @@ def encode(prog: Program) -> None:
         group_w.append(
             [g.arity, int(g.diag), int(g.perrow), len(g.gates), g0, wa, wb,
              prog.slot_base.get(g.gid, -1), g.slot_floats, g.mat_floats, int(g.needs_grad),
-             0, 0, 0, 0, 0]
+             rowidx if g.perrow else -1, 0, 0, 0, 0]
         )
+        rowidx += int(g.perrow)
     pass_w, phase_w, op_w, sub_w, pgrp_w = [], [], [], [], []
+    prog.enc = []
+    prog.rowidx = {}
+    ri = 0
+    for g in prog.groups:
+        if g.perrow:
+            prog.rowidx[g.gid] = ri
+            ri += 1
     for pi, pp in enumerate(prog.passes):
         # per-pass shared-memory tables: group matrices, coupling slots (float offsets)
         mat_off, slot_off = {}, {}
@@ -492,6 +571,9 @@ def encode(prog: Program) -> None:
             tile_mask |= 1 << p
         ph0 = len(phase_w)
         first_slot = min((prog.slot_base[g] for g in pp.groups if g in prog.slot_base), default=0)
+        enc = {"ops": [], "subs": sub_w, "matf": mo, "slotf": so,
+               "pgroups": [(gid, mat_off[gid]) for gid in pp.groups]}
+        prog.enc.append(enc)
         for ph in pp.phases:
             op0 = len(op_w)
             reg_of_local = {b: k for k, b in enumerate(ph.regs)}
@@ -499,6 +581,16 @@ def encode(prog: Program) -> None:
             i = 0
             while i < len(ops):
                 g = prog.groups[ops[i]]
+                perm = g.perm_ops if not g.diag else None
+                if perm is not None:
+                    regs_of = [reg_of_local[pp.local_of_phys[n - 1 - w]] for w in g.wires]
+                    for p in perm:
+                        if p[0] == "x":
+                            op_w.append([OP_PX, regs_of[p[1]], -1, g.gid, -1, -1, 0, 0])
+                        else:
+                            op_w.append([OP_PCX, regs_of[p[1]], regs_of[p[2]], g.gid, -1, -1, 0, 0])
+                    i += 1
+                    continue
                 if not g.diag:
                     if g.arity == 1:
                         a = reg_of_local[pp.local_of_phys[n - 1 - g.wires[0]]]
@@ -531,6 +623,7 @@ def encode(prog: Program) -> None:
                     sub_w.append([srcs[0], srcs[1], gd.gid, mat_off[gd.gid], slot_off.get(gd.gid, -1), gd.arity, 0, 0])
                     i += 1
                 op_w.append([OP_DRUN, -1, -1, -1, -1, -1, s0, len(sub_w) - s0])
+            enc["ops"].append([list(r) for r in op_w[op0:]])
             regs = list(ph.regs) + [0] * (MAX_R - len(ph.regs))
             thr = list(ph.threads) + [0] * (16 - len(ph.threads))
             phase_w.append(regs + thr + [op0, len(op_w) - op0, 0])
@@ -552,6 +645,7 @@ def encode(prog: Program) -> None:
     hdr[5] = prog.slot_total
     hdr[6] = len(prog.passes)
     hdr[7] = len(prog.groups)
+    hdr[22] = rowidx  # number of per-row (encoding) groups
     off = HDR_WORDS
     flat = []
     for si, (sec, wd) in enumerate(zip(sections, widths)):

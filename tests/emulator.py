@@ -135,6 +135,21 @@ class Emulator:
             v[:, :, idx[r]] = acc
 
     @staticmethod
+    def _perm_local(v, kind, a, b=None):
+        """X on local bit a, or CX local a -> local b (register-permutation ops)."""
+        D = v.shape[2]
+        L = np.arange(D)
+        if kind == S.OP_PX:
+            sel = L[_bit(L, a) == 0]
+            dst = sel | (1 << a)
+        else:
+            sel = L[(_bit(L, a) == 1) & (_bit(L, b) == 0)]
+            dst = sel | (1 << b)
+        t = v[:, :, sel].copy()
+        v[:, :, sel] = v[:, :, dst]
+        v[:, :, dst] = t
+
+    @staticmethod
     def _coupling(lam, psi, bits):
         B, Tn, D = psi.shape
         L = np.arange(D)
@@ -199,7 +214,9 @@ class Emulator:
             regs = phase[:5]
             for op in ops_of(phase):
                 kind = int(op[0])
-                if kind == S.OP_U1:
+                if kind in (S.OP_PX, S.OP_PCX):
+                    self._perm_local(P, kind, int(regs[op[1]]), int(regs[op[2]]) if kind == S.OP_PCX else None)
+                elif kind == S.OP_U1:
                     U = group_unitary(self.w, self.fv, theta, x, int(op[3]))
                     self._apply_local(P, U, [int(regs[op[1]])])
                 elif kind == S.OP_U2:
@@ -220,7 +237,10 @@ class Emulator:
             for op in ops_of(phase)[::-1]:
                 kind = int(op[0])
                 gid = int(op[3]) if int(op[0]) != S.OP_DRUN else -1
-                if kind in (S.OP_U1, S.OP_U2):
+                if kind in (S.OP_PX, S.OP_PCX):
+                    for v in (Pv, Lv):
+                        self._perm_local(v, kind, int(regs[op[1]]), int(regs[op[2]]) if kind == S.OP_PCX else None)
+                elif kind in (S.OP_U1, S.OP_U2):
                     bits = [int(regs[op[1]])] + ([int(regs[op[2]])] if kind == S.OP_U2 else [])
                     grp = self.groups[gid]
                     if int(grp[10]):
