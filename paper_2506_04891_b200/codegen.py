@@ -168,13 +168,13 @@ def _emit_small(w, v, U, q):
         expr = None
         for c in range(d):
             a, b = float(np.real(U[r, c])), float(np.imag(U[r, c]))
-            for coef, arg in ((a, f"x{c}"), (b, f"jx(x{c})")):
+            for coef, kind in ((a, "x"), (b, "ix")):
                 if abs(coef) < 1e-15:
                     continue
                 if expr is None:
-                    expr = f"f2mul({arg}, bc({_f(coef)}))"
+                    expr = f"{'mx' if kind == 'x' else 'mix'}(x{c}, {_f(coef)})"
                 else:
-                    expr = f"f2fma({arg}, bc({_f(coef)}), {expr})"
+                    expr = f"{'fx' if kind == 'x' else 'fix'}(x{c}, {_f(coef)}, {expr})"
         w(f"  {v}[{q[r]}] = {expr if expr else 'make_float2(0.f, 0.f)'};")
     w("}")
 
@@ -366,11 +366,14 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
     w(f"float* s_mat = reinterpret_cast<float*>(s_x + {1 << P.M});")
     w(f"float* s_acc = s_mat + {(matf + 3) & ~3};")
     w(f"double* s_z = reinterpret_cast<double*>(s_acc + {(P.NW * slotf + 3) & ~3});")
-    w("float* s_red = reinterpret_cast<float*>(s_z + 34);")
+    w("float* s_zw = reinterpret_cast<float*>(s_z + 34);  // [NW][32] per-warp <Z> partials")
+    # next-tile prefetch stage [NV][2^M], natural local order, after the fixed tables so the
+    # generic kernel's shared-memory size plus NV x 2^M x 8 B covers it (lsq_program_jit)
+    w(f"float2* s_stage = reinterpret_cast<float2*>((reinterpret_cast<size_t>(s_zw + {P.NW * 32}) + 15) & ~(size_t)15);")
     w("const int tid = threadIdx.x, warp = tid >> 5;")
     w("const int row = blockIdx.x / A.ctas_per_row, cslot = blockIdx.x % A.ctas_per_row;")
     w("const int mode = A.mode, flags = A.flags;")
-    w("(void)mode; (void)warp; (void)s_red;")
+    w("(void)mode; (void)warp; (void)s_zw;")
     # stage group tables
     pgs = P.enc["pgroups"]  # list of (gid, moff)
     w("{")
@@ -386,6 +389,7 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
             w(f"for (int e = tid; e < {grp.mat_floats}; e += NT) s_mat[{moff} + e] = A.gmats[{gid * 32} + e];")
     w(f"for (int i = tid; i < {P.NW * slotf}; i += NT) s_acc[i] = 0.f;")
     w("for (int i = tid; i < 34; i += NT) s_z[i] = 0.0;")
+    w(f"for (int i = tid; i < {P.NW * 32}; i += NT) s_zw[i] = 0.f;")
     w.ind -= 1
     w("}")
     w("__syncthreads();")
@@ -400,8 +404,50 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
         w(f"const uint32_t st{k} = swz(tp{k});")
         w(f"(void)tp{k}; (void)gt{k}; (void)st{k};")
     w(f"const size_t rowbase = (size_t)row << {P.n};")
-    w("const int t0 = cslot * A.tiles_per_cta;")
-    w.block("for (int t = t0; t < t0 + A.tiles_per_cta; ++t)")
+    w("const int t0 = cslot * A.tiles_per_cta, t_end = t0 + A.tiles_per_cta;")
+    last = nph - 1
+    # ---- next-tile prefetch: cp.async 16-byte chunks into the stage (natural local order).
+    # chunk c holds local amplitudes (2c, 2c+1); c = (tid low bits) + j * 2^tid_bits.
+    nchunk = 1 << (P.M - 1)
+    per_thr = max(1, nchunk // P.NT)
+    tid_bits = (nchunk // per_thr).bit_length() - 1
+    cth_terms = [f"(((uint32_t)tid >> {jj}) & 1u) << {P.pbit[jj + 1]}" for jj in range(tid_bits)]
+    w(f"const uint32_t cth = {' | '.join(cth_terms) if cth_terms else '0u'};")
+    w(f"const bool cp_on = tid < {nchunk};")
+    w("(void)cth; (void)cp_on;")
+    ld_vecs = [(0, "A.psi_in"), (1, "A.lam")] if mode == MODE_BWD else [(0, "A.psi_in")]
+    if mode == MODE_FWD:
+        w("const bool do_load = !(flags & PF_SYNTH);")
+    elif mode == MODE_BWD:
+        w("const bool do_load = true;")
+    else:
+        w("const bool nofwd = (flags & PF_NOFWD) != 0;")
+        w("const bool do_load = nofwd || !(flags & PF_SYNTH);")
+
+    def emit_issue(tile_expr):
+        tb2 = [f"((uint64_t)((({tile_expr}) >> {jj}) & 1)) << {p}" for jj, p in enumerate(P.nbit)]
+        w.block("if (cp_on)")
+        w(f"const size_t nb = rowbase + ({' | '.join(tb2) if tb2 else '0ull'});")
+        for vi, ptr in ld_vecs:
+            for jj in range(per_thr):
+                loc = 2 * (jj << tid_bits)
+                phys = sum(1 << P.pbit[b] for b in range(P.M) if (loc >> b) & 1)
+                w(f"cp_async16(s_stage + {vi * (1 << P.M) + loc} + 2 * (tid & {(1 << tid_bits) - 1}), "
+                  f"{ptr} + nb + (cth | {phys}u));")
+        w.end()
+
+    def emit_stage_read(k):
+        ph = P.pp.phases[k]
+        for vi, _ in ld_vecs:
+            for i in range(P.NR):
+                loc = sum(1 << ph.regs[b] for b in range(P.R) if (i >> b) & 1)
+                w(f"v[{vi}][{i}] = s_stage[{vi * (1 << P.M)} + (tp{k} | {loc}u)];")
+
+    w.block("if (do_load && t0 < t_end)")
+    emit_issue("t0")
+    w.end()
+    w("cp_async_commit();")
+    w.block("for (int t = t0; t < t_end; ++t)")
     tb = [f"((uint64_t)((t >> {j}) & 1)) << {p}" for j, p in enumerate(P.nbit)]
     w(f"const uint64_t tbase = {' | '.join(tb) if tb else '0ull'};")
     # opaque per-tile copies of the shared-memory thread offsets: keeps the 2^R swizzled
@@ -410,23 +456,23 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
         w(f"uint32_t sx{k} = st{k}; asm volatile(\"\" : \"+r\"(sx{k}));")
     w("const size_t base = rowbase + tbase;")
     w(f"float2 v[{nv}][{P.NR}];")
-    last = nph - 1
-    nofwd = mode == MODE_BWD
-    if mode == MODE_TURN:
-        w("const bool nofwd = (flags & PF_NOFWD) != 0;")
-    first_expr = {MODE_FWD: "0", MODE_BWD: str(last)}.get(mode)
 
-    def emit_load(k, synth_ok):
-        if synth_ok:
-            w.block("if (flags & PF_SYNTH)")
-            for i in range(P.NR):
-                w(f"v[0][{i}] = make_float2(((tbase | (uint64_t)(gt{k} | {P.goff(k, i)}u)) == 0) ? 1.f : 0.f, 0.f);")
-            w.end()
-            w.block("else")
+    def emit_load(k):
+        """wait for this tile's prefetch, move it to registers (layout k), prefetch the next"""
+        w.block("if (do_load)")
+        w("cp_async_wait_all();")
+        w("__syncthreads();")
+        emit_stage_read(k)
+        w("__syncthreads();")
+        w.block("if (t + 1 < t_end)")
+        emit_issue("t + 1")
+        w.end()
+        w("cp_async_commit();")
+        w.end()
+
+    def emit_synth(k):
         for i in range(P.NR):
-            w(f"v[0][{i}] = __ldcs(A.psi_in + base + (gt{k} | {P.goff(k, i)}u));")
-        if synth_ok:
-            w.end()
+            w(f"v[0][{i}] = make_float2(((tbase | (uint64_t)(gt{k} | {P.goff(k, i)}u)) == 0) ? 1.f : 0.f, 0.f);")
 
     def emit_fwd_phases():
         for k in range(nph):
@@ -435,6 +481,9 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
                 _emit_exchange(w, P, k, k + 1, nv)
 
     def emit_zpart(k):
+        # <Z> partials without block barriers: warp shuffle tree, then lane 0 of each warp adds
+        # into its own per-warp slot (indexed by physical bit; [n] = norm). Reduced over warps in
+        # fp64 once per CTA, after the tile loop.
         ph = P.pp.phases[k]
         w("{")
         w.ind += 1
@@ -452,18 +501,14 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
         for j, lb in enumerate(ph.threads):
             w(f"pz[{lb}] += ((tp{k} >> {lb}) & 1u) ? -S_ : S_;")
         w(f"warp_sum<NT, {P.M + 1}>(pz);")
-        w(f"if ((tid & 31) == 0) {{ for (int e = 0; e <= {P.M}; ++e) s_red[warp * {P.M + 1} + e] = pz[e]; }}")
-        w("__syncthreads();")
-        w.block("if (tid == 0)")
-        w(f"double tot[{P.M + 1}];")
-        w(f"for (int e = 0; e <= {P.M}; ++e) {{ double s = 0.0; for (int ww = 0; ww < NW; ++ww) s += (double)s_red[ww * {P.M + 1} + e]; tot[e] = s; }}")
+        w.block("if ((tid & 31) == 0)")
+        w(f"float* zw = s_zw + warp * 32;")
         for e, p in enumerate(P.pbit):
-            w(f"s_z[{p}] += tot[{e}];")
+            w(f"zw[{p}] += pz[{e}];")
         for p in P.nbit:
-            w(f"s_z[{p}] += ((tbase >> {p}) & 1ull) ? -tot[{P.M}] : tot[{P.M}];")
-        w(f"s_z[{P.n}] += tot[{P.M}];")
+            w(f"zw[{p}] += ((tbase >> {p}) & 1ull) ? -pz[{P.M}] : pz[{P.M}];")
+        w(f"zw[{P.n}] += pz[{P.M}];")
         w.end()
-        w("__syncthreads();")
         w.ind -= 1
         w("}")
 
@@ -506,27 +551,32 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
             w.end()
 
     if mode == MODE_FWD:
-        emit_load(0, True)
+        emit_load(0)
+        w.block("if (!do_load)")
+        emit_synth(0)
+        w.end()
         emit_fwd_phases()
         w.block("if (flags & PF_ZPART)")
         emit_zpart(last)
         w.end()
         emit_store(last, "psi")
     elif mode == MODE_BWD:
-        emit_load(last, False)
-        for i in range(P.NR):
-            w(f"v[1][{i}] = __ldcs(A.lam + base + (gt{last} | {P.goff(last, i)}u));")
+        emit_load(last)
         emit_bwd_phases()
         emit_store(0, "psi")
         emit_store(0, "lam")
     else:
         # turnaround: forward phases (unless NOFWD), <Z>, lambda = O psi, adjoint phases
         w.block("if (nofwd)")
-        for i in range(P.NR):
-            w(f"v[0][{i}] = __ldcs(A.psi_in + base + (gt{last} | {P.goff(last, i)}u));")
+        emit_load(last)
         w.end()
         w.block("else")
-        emit_load(0, True)
+        w.block("if (do_load)")
+        emit_load(0)
+        w.end()
+        w.block("else")
+        emit_synth(0)
+        w.end()
         emit_fwd_phases()
         w.end()
         emit_zpart(last)
@@ -544,7 +594,7 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
         w.end()
     w.block(f"if ((mode == PMODE_TURN || (flags & PF_ZPART)) && A.zpart)")
     w(f"double* dst = A.zpart + (size_t)blockIdx.x * {P.n + 1};")
-    w(f"for (int f = tid; f <= {P.n}; f += NT) dst[f] = s_z[f];")
+    w(f"for (int f = tid; f <= {P.n}; f += NT) {{ double s = 0.0; for (int ww = 0; ww < NW; ++ww) s += (double)s_zw[ww * 32 + f]; dst[f] = s; }}")
     w.end()
     out.extend(w.lines)
     out.append("}")

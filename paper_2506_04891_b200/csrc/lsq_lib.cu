@@ -169,12 +169,20 @@ __global__ void k_zero(double* p, int64_t n) {
     p[i] = 0.0;
 }
 
-// grad_sum[t] = sum_b grows[b][t], fixed order
+// grad_sum[t] = sum_b grows[b][t]: one block per t, fixed-shape tree (deterministic)
 __global__ void k_sum_rows(const double* grows, int batch, int T, double* out) {
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += gridDim.x * blockDim.x) {
+  __shared__ double red[256];
+  for (int t = blockIdx.x; t < T; t += gridDim.x) {
     double s = 0.0;
-    for (int b = 0; b < batch; ++b) s += grows[(size_t)b * T + t];
-    out[t] = s;
+    for (int b = threadIdx.x; b < batch; b += blockDim.x) s += grows[(size_t)b * T + t];
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+      if ((int)threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) out[t] = red[0];
+    __syncthreads();
   }
 }
 
@@ -242,7 +250,7 @@ size_t smem_bytes(const lsq_program* P, const PassInfo& pi, int NV) {
   b += sizeof(int) * ((size_t)pi.nph * PHASE_WORDS + (size_t)pi.nops * OP_WORDS + (size_t)pi.nsubs * SUB_WORDS + 64);
   b += sizeof(float) * (((pi.matf + 3) & ~3) + ((NW * pi.slotf + 3) & ~3));
   b += sizeof(double) * 34;
-  b += sizeof(float) * NW * (pi.M + 1);
+  b += sizeof(float) * NW * 32;  // per-warp <Z> / reduction scratch (n + 1 <= 32, M + 1 <= 32)
   return (b + 15) & ~(size_t)15;
 }
 
@@ -353,9 +361,9 @@ int launch_pass(lsq_program* P, int pi_idx, int mode, int flags, int batch, cons
   A.wts = w;
   A.part = ws.part;
   A.zpart = ws.zpart;
-  const size_t sm = smem_bytes(P, pi, NV);
   const JitKernel* jk = nullptr;
   if (!P->jit.empty() && P->jit[pi_idx * 3 + mode].fn) jk = &P->jit[pi_idx * 3 + mode];
+  const size_t sm = jk ? jk->smem_set : smem_bytes(P, pi, NV);
   if (P->profiling) {
     while ((int)P->ev.size() < 2 * (P->ev_used + 1)) {
       cudaEvent_t e;
@@ -410,7 +418,7 @@ int finish_grads(lsq_program* P, int batch, const double* theta, const double* x
     CUDA_TRY(cudaGetLastError());
   }
   if (grad_sum && P->T) {
-    k_sum_rows<<<(P->T + 127) / 128, 128, 0, st>>>(grows, batch, P->T, grad_sum);
+    k_sum_rows<<<std::min(P->T, 4096), 256, 0, st>>>(grows, batch, P->T, grad_sum);
     P->launches++;
     CUDA_TRY(cudaGetLastError());
   }
@@ -599,7 +607,9 @@ int lsq_program_jit(lsq_program* P, int nk, const char* const* sources, const in
     jk.fn = (const void*)kern;
     const PassInfo& pi = P->passes[pass_idx[i]];
     jk.NT = 1 << (pi.M - pi.R);
-    const size_t sm = smem_bytes(P, pi, modes[i] == 0 ? 1 : 2);
+    // specialised kernels add a next-tile prefetch stage of NV x 2^M amplitudes
+    const int NV = modes[i] == 0 ? 1 : 2;
+    const size_t sm = smem_bytes(P, pi, NV) + (size_t)NV * sizeof(float2) * ((size_t)1 << pi.M);
     CUDA_TRY(cudaFuncSetAttribute(jk.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     jk.smem_set = sm;
   }

@@ -126,10 +126,17 @@ class Engine:
             raise ValueError("the engine runs on CUDA devices only")
         self.circuit = circuit
         self.n = int(circuit.n)
-        self.program = compile_circuit(circuit, M=M, R=R)
-        self.native = NativeProgram(self.program, self.device)
         if jit is None:
             jit = os.environ.get("LSQ_JIT", "1") != "0"
+        if jit and R is None:
+            # specialised kernels: 16 amplitudes per thread per vector once tiles are >= 9
+            # bits (measured best, profiles/r01); the generic kernels keep schedule.default_r
+            from .schedule import DEFAULT_M, DEFAULT_R_SPECIALISED, default_r
+
+            m = min(self.n, M if M is not None else DEFAULT_M)
+            R = DEFAULT_R_SPECIALISED if m >= 9 else default_r(m)
+        self.program = compile_circuit(circuit, M=M, R=R)
+        self.native = NativeProgram(self.program, self.device)
         if jit:
             self.native.attach_jit()
         self.variant = "jit" if jit else "interp"

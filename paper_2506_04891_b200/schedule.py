@@ -41,6 +41,10 @@ COAL = 4  # low physical bits always inside a tile (16 amplitudes = one 128 B li
 MAX_R = 5  # register bits per thread (2^5 = 32 amplitudes per vector per thread)
 MAX_M_FWD = 14
 MAX_M_BWD = 13
+# measured on B200 (profiles/r01/sweep_c2_*.log): 12 tile bits with 16 amplitudes per thread
+# per vector balances passes (HBM) against occupancy/exchanges best for the adjoint kernels
+DEFAULT_M = 12
+DEFAULT_R_SPECIALISED = 4
 ENC_FLAG = 1 << 30  # param source tag: encoding column
 FIXED_SRC = -1
 
@@ -488,7 +492,7 @@ def compile_circuit(circuit, M: int | None = None, R: int | None = None) -> Prog
     groups = fuse_groups(gates)
     preds = group_preds(groups)
     if M is None:
-        M = min(n, MAX_M_BWD)
+        M = min(n, DEFAULT_M)
     M = min(M, n)
     passes = schedule_passes(groups, n, M)
     need2 = any(g.arity == 2 and not g.diag for g in groups)

@@ -1,7 +1,8 @@
 #!/bin/bash
 # Tile-bits / register-bits sweep of the default workload (cfg2) -- numbers for DESIGN.md.
 CFG=${1:-2}
-for MR in "13 5" "13 4" "12 4" "12 5" "11 4" "11 3"; do
+IFS=, read -ra LIST <<< "${MRS:-13 5,13 4,12 4,11 4,11 3,10 5,9 4,10 4}"
+for MR in "${LIST[@]}"; do
   set -- $MR
   python bench.py --config $CFG --steps 5 --warmup 3 --no-cpu --M $1 --R $2 > gpurun_out/sweep_c${CFG}_M$1_R$2.log 2>&1
   python - "$1" "$2" "gpurun_out/sweep_c${CFG}_M$1_R$2.log" <<'PY'
