@@ -159,21 +159,39 @@ def run_reference(args, world, rank):
 
 
 class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 20 ms while the timed region runs.
+    Samples are time-stamped and kept if they fall inside [mark_start, mark_end] (+-150 ms
+    when the region is shorter than the sampling period)."""
+
+    FIELDS = ("timestamp,index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
     def __init__(self, gpu_indices):
         self.idx = ",".join(str(i) for i in gpu_indices)
         self.proc = None
+        self.t0 = self.t1 = None
 
     def __enter__(self):
-        q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", self.idx, f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                ["nvidia-smi", "-i", self.idx, f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.3)  # let the sampler start before the timed region
         except Exception:
             self.proc = None
         return self
+
+    def mark_start(self):
+        import datetime
+
+        self.t0 = datetime.datetime.now()
+
+    def mark_end(self):
+        import datetime
+
+        self.t1 = datetime.datetime.now()
+        time.sleep(0.05)
 
     def __exit__(self, *a):
         self.lines = []
@@ -186,24 +204,35 @@ class ClockSampler:
             self.lines = [l for l in out.splitlines() if l.strip()]
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
+        import datetime
+
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        samples = []
         for l in getattr(self, "lines", []):
             p = [x.strip() for x in l.split(",")]
-            if len(p) < 8:
+            if len(p) < 9:
                 continue
             try:
-                sm.append(float(p[1]))
-                mx = float(p[2])
+                ts = datetime.datetime.strptime(p[0], "%Y/%m/%d %H:%M:%S.%f")
+                samples.append((ts, float(p[2]), float(p[3]), p[5:9]))
             except ValueError:
                 continue
-            for nm, v in zip(names, p[4:8]):
+        if not samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        win = samples
+        if self.t0 and self.t1:
+            inside = [x for x in samples if self.t0 <= x[0] <= self.t1]
+            if not inside:
+                pad = datetime.timedelta(milliseconds=150)
+                inside = [x for x in samples if self.t0 - pad <= x[0] <= self.t1 + pad]
+            win = inside or samples
+        reasons = set()
+        for x in win:
+            for nm, v in zip(names, x[3]):
                 if v.lower() == "active":
                     reasons.add(nm)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        return {"sm_mhz": statistics.median(x[1] for x in win), "sm_max_mhz": max(x[2] for x in win),
+                "reasons": sorted(reasons), "samples": len(win)}
 
 
 def _pass_vectors(prog, mode, pidx):
@@ -264,12 +293,14 @@ def run_ours(args, world, rank, local):
     nchunks = (b + mb - 1) // mb
     with ClockSampler([local] if world == 1 else list(range(world))) as clk:
         barrier()
+        clk.mark_start()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(args.steps):
             step()
         e1.record()
         barrier()
+        clk.mark_end()
     ms = e0.elapsed_time(e1)
     if world > 1:
         import torch.distributed as dist
@@ -284,12 +315,12 @@ def run_ours(args, world, rank, local):
     per_kernel = {}
     nprof = max(2, min(args.steps, 5))
     for _ in range(nprof):
+        eng.native.profile = []
         eng.fwd_bwd(theta, x, batch=b, weights=w, rows=False, encoding_grads=False, micro_batch=mb,
                     buffers=bufs)
-        for kind, t in eng.native.pass_times():
+        for kind, t, rows_launch in eng.native.profile:
             mode, pidx = divmod(kind, 1000)
             vec = _pass_vectors(eng.program, mode, pidx)
-            rows_launch = mb  # every launch covers one micro-batch
             key = "lsq_pass_kernel<M=%d,NV=%d>" % (eng.program.passes[pidx].M, 1 if mode == 0 else 2)
             d = per_kernel.setdefault(key, {"bytes": 0.0, "ms": 0.0, "launches": 0})
             d["bytes"] += vec * rows_launch * (8 << n)

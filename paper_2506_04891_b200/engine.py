@@ -59,6 +59,8 @@ class NativeProgram:
         self.handle = h
         self._ws = {}
         self.jit = False
+        self.profiling = False
+        self.profile = []
 
     def attach_jit(self, cache_dir=None):
         """Compile the per-pass specialised kernels (codegen.py) with NVRTC for sm_100a."""
@@ -105,6 +107,8 @@ class NativeProgram:
 
     def set_profiling(self, on: bool):
         _native.check(_native.lib().lsq_set_profiling(self.handle, int(on)))
+        self.profiling = bool(on)
+        self.profile = []  # (kind, ms, rows) for every pass launch since profiling was enabled
 
     def pass_times(self):
         cap = 4096
@@ -165,13 +169,23 @@ class Engine:
         return nvec * (8 << self.n)
 
     def micro_batch(self, batch: int, nvec: int) -> int:
+        # cudaMemGetInfo costs ~4 ms per call on B200: query once per (batch, nvec)
+        key = (batch, nvec)
+        cache = self.__dict__.setdefault("_mb_cache", {})
+        if key in cache:
+            return cache[key]
         free, _ = torch.cuda.mem_get_info(self.device)
-        cap = int(free * _STATE_FRACTION) // self.row_bytes(nvec)
+        # buffers this engine already holds for a previous call count as available
+        held = 0
+        for t in self.__dict__.get("_held_buffers", ()):
+            held += t.numel() * t.element_size()
+        cap = int((free + held) * _STATE_FRACTION) // self.row_bytes(nvec)
         if cap < 1:
             raise CapacityError(
                 f"one row of 2^{self.n} amplitudes x {nvec} vectors does not fit in device memory"
             )
-        return min(batch, cap)
+        cache[key] = min(batch, cap)
+        return cache[key]
 
     # -- forward ----------------------------------------------------------------------------
     def forward(self, trainable=None, encoding=None, state=None, batch=None, weights=None, want_z=False):
@@ -218,11 +232,15 @@ class Engine:
         erows = torch.empty((batch, self.E), **f64) if (encoding_grads and self.E) else None
         nchunk = (batch + mb - 1) // mb
         gparts = torch.zeros((nchunk, max(self.T, 1)), **f64)
+        held = self.__dict__.get("_held_buffers")
         if buffers is not None and buffers[0].shape[0] >= mb:
             psi, lam = buffers
+        elif held is not None and held[0].shape[0] >= mb:
+            psi, lam = held
         else:
             psi = torch.empty((mb, 1 << self.n), dtype=torch.complex64, device=dev)
             lam = torch.empty_like(psi)
+            self._held_buffers = (psi, lam)
         ws = self.native.workspace(mb)
         lib = _native.lib()
         for c in range(nchunk):
@@ -239,6 +257,8 @@ class Engine:
                     ws.data_ptr(), self._stream(),
                 )
             )
+            if self.native.profiling:
+                self.native.profile += [(k, ms, b) for k, ms in self.native.pass_times()]
         gsum = gparts.sum(dim=0)[: self.T] if nchunk > 1 else gparts[0, : self.T]
         return {"value": value, "zq": zq, "grads": grows, "grad_sum": gsum, "encoding_grads": erows,
                 "buffers": (psi, lam)}
@@ -271,7 +291,8 @@ class Engine:
                 "encoding_grads": erows[:, : self.E]}
 
 
-_CACHE: dict = {}
+_CACHE: "OrderedDict" = None
+_CACHE_MAX = 8  # engines (programs + held state buffers) kept alive, least recently used evicted
 
 
 def engine_for(circuit, device=None, M=None, R=None, jit=None) -> Engine:
@@ -279,11 +300,20 @@ def engine_for(circuit, device=None, M=None, R=None, jit=None) -> Engine:
     dev = torch.device(device if device is not None else "cuda")
     if dev.type == "cuda" and dev.index is None:
         dev = torch.device("cuda", torch.cuda.current_device())
+    global _CACHE
+    if _CACHE is None:
+        from collections import OrderedDict
+
+        _CACHE = OrderedDict()
     key = (_circuit_key(circuit), M, R, jit, str(dev))
     eng = _CACHE.get(key)
     if eng is None:
         eng = Engine(circuit, M=M, R=R, device=dev, jit=jit)
         _CACHE[key] = eng
+        while len(_CACHE) > _CACHE_MAX:
+            _CACHE.popitem(last=False)
+    else:
+        _CACHE.move_to_end(key)
     return eng
 
 
