@@ -49,9 +49,12 @@ def _dist_env():
     return world, rank, local
 
 
-def _workload_rows(cfg, world, rank):
+def _workload_rows(cfg, world, rank, batch=None):
     """(workload, start, stop, global_batch, scaling) for this rank."""
     n, b = CONFIG_SHAPES[cfg]
+    if batch is not None:  # experiments only: reduced batch of the same circuit
+        wl = make_workload(cfg, batch=batch * world)
+        return wl, rank * batch, (rank + 1) * batch, batch * world, "weak"
     if cfg == 5:  # BASELINE: 1024 rows sharded over the GPUs
         from paper_2506_04891_b200.distributed import shard_rows
 
@@ -235,14 +238,16 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(win)}
 
 
-def _pass_vectors(prog, mode, pidx):
+def _pass_vectors(prog, mode, pidx, adjoint="recompute"):
     """State-vector transfers (reads + writes of one (rows, 2^n) vector) of one launch."""
     L = len(prog.passes)
     if mode == 0:  # forward: read psi (not for the synthesized first pass) + write psi
         return (0 if pidx == 0 else 1) + 1
     if mode == 1:  # turnaround: read psi (unless synthesized), write lambda (unless last)
         return (0 if L == 1 else 1) + (1 if L > 1 else 0)
-    return 2 + (2 if pidx > 0 else 0)  # adjoint: read psi, lambda; write both unless pass 0
+    # adjoint: read psi, lambda; write lambda (+ psi when un-computing) unless pass 0
+    writes = 0 if pidx == 0 else (1 if adjoint == "ckpt" else 2)
+    return 2 + writes
 
 
 def run_ours(args, world, rank, local):
@@ -258,20 +263,19 @@ def run_ours(args, world, rank, local):
 
         dist.init_process_group("nccl", device_id=dev)
     cfg = args.config
-    wl, r0, r1, gbatch, scaling = _workload_rows(cfg, world, rank)
+    wl, r0, r1, gbatch, scaling = _workload_rows(cfg, world, rank, args.batch)
     b = r1 - r0
     n = wl.n
     eng = Engine(wl.circuit, device=dev, M=args.M, R=args.R)
     theta = torch.as_tensor(wl.theta, device=dev)
     x = torch.as_tensor(wl.x[r0:r1], device=dev)
     w = torch.as_tensor(wl.weights, device=dev)
-    mb = eng.micro_batch(b, 2)
     bufs = None
 
     def step():
         nonlocal bufs
         r = eng.fwd_bwd(theta, x, batch=b, weights=w, rows=False, encoding_grads=False,
-                        micro_batch=mb, buffers=bufs)
+                        buffers=bufs, checkpoint=None if args.checkpoint is None else bool(args.checkpoint))
         bufs = r["buffers"]
         if world > 1:
             import torch.distributed as dist
@@ -290,6 +294,7 @@ def run_ours(args, world, rank, local):
         step()
     barrier()
     launches = eng.native.launch_count()
+    mb = eng.last_micro_batch
     nchunks = (b + mb - 1) // mb
     with ClockSampler([local] if world == 1 else list(range(world))) as clk:
         barrier()
@@ -317,10 +322,10 @@ def run_ours(args, world, rank, local):
     for _ in range(nprof):
         eng.native.profile = []
         eng.fwd_bwd(theta, x, batch=b, weights=w, rows=False, encoding_grads=False, micro_batch=mb,
-                    buffers=bufs)
+                    buffers=bufs, checkpoint=None if args.checkpoint is None else bool(args.checkpoint))
         for kind, t, rows_launch in eng.native.profile:
             mode, pidx = divmod(kind, 1000)
-            vec = _pass_vectors(eng.program, mode, pidx)
+            vec = _pass_vectors(eng.program, mode, pidx, eng.last_adjoint)
             key = "lsq_pass_kernel<M=%d,NV=%d>" % (eng.program.passes[pidx].M, 1 if mode == 0 else 2)
             d = per_kernel.setdefault(key, {"bytes": 0.0, "ms": 0.0, "launches": 0})
             d["bytes"] += vec * rows_launch * (8 << n)
@@ -400,7 +405,8 @@ def run_ours(args, world, rank, local):
         "scaling": scaling, "vs_baseline": None, "dtype": "c64 (fp32 complex; fp64 reductions)",
         "data": "synthetic (seeded BASELINE inputs, A5 draw order)",
         "config": {"workload": CONFIG_NAMES[cfg], "n_qubits": n, "global_batch": gbatch,
-                   "rows_per_gpu": b, "micro_batch": mb, "parallelism": f"dp{world}",
+                   "rows_per_gpu": b, "micro_batch": mb, "adjoint": eng.last_adjoint,
+                   "parallelism": f"dp{world}",
                    "passes": len(eng.program.passes), "tile_bits": eng.program.passes[0].M,
                    "reg_bits": eng.program.passes[0].R, "variant": eng.variant,
                    "l2": f"working set {2 * b * (8 << n) / 2**20:.0f} MiB (psi+lambda) vs 126 MB L2"
@@ -429,6 +435,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--M", type=int, default=None, help="tile bits per pass (default: planner/engine)")
     ap.add_argument("--R", type=int, default=None, help="register bits per thread")
+    ap.add_argument("--batch", type=int, default=None, help="experiments: rows per GPU (not a bench line)")
+    ap.add_argument("--checkpoint", type=int, default=None, choices=[0, 1],
+                    help="adjoint with forward checkpoints (1) or in-place un-computation (0); default: engine")
     args = ap.parse_args()
     world, rank, local = _dist_env()
     if args.impl == "reference":

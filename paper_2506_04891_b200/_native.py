@@ -33,6 +33,7 @@ _SIGS = {
     "lsq_workspace_bytes": (_I64, [_P, _I]),
     "lsq_forward": (_I, [_P, _I, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P]),
     "lsq_fwd_bwd": (_I, [_P, _I, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "lsq_fwd_bwd_ckpt": (_I, [_P, _I, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "lsq_bwd_from_state": (_I, [_P, _I, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "lsq_set_profiling": (_I, [_P, _I]),
     "lsq_last_pass_times": (_I, [_P, _P, _I, _P]),

@@ -702,6 +702,14 @@ int lsq_forward(const lsq_program* Pc, int batch, const double* theta, const dou
 int lsq_fwd_bwd(const lsq_program* Pc, int batch, const double* theta, const double* x, int x_stride,
                 const double* w, void* psi_v, void* lam_v, double* zq, double* value, double* grad_rows,
                 double* grad_sum, double* egrad_rows, void* workspace, void* stream) {
+  return lsq_fwd_bwd_ckpt(Pc, batch, theta, x, x_stride, w, psi_v, lam_v, nullptr, zq, value, grad_rows,
+                          grad_sum, egrad_rows, workspace, stream);
+}
+
+int lsq_fwd_bwd_ckpt(const lsq_program* Pc, int batch, const double* theta, const double* x, int x_stride,
+                     const double* w, void* psi_v, void* lam_v, void* ckpt_v, double* zq, double* value,
+                     double* grad_rows, double* grad_sum, double* egrad_rows, void* workspace,
+                     void* stream) {
   auto* P = const_cast<lsq_program*>(Pc);
   if (!P || batch < 1 || !psi_v || !lam_v || !workspace) return fail(LSQ_EINVAL, "null argument");
   if (P->T && !theta) return fail(LSQ_EINVAL, "circuit has trainable parameters but none given");
@@ -726,14 +734,21 @@ int lsq_fwd_bwd(const lsq_program* Pc, int batch, const double* theta, const dou
   k_zero<<<(int)std::min<int64_t>((mtot + 255) / 256, 4096), 256, 0, st>>>(ws.macc, mtot);
   P->launches++;
   const int L = P->npasses;
+  // checkpoint mode: pass i writes its output to ckpt[i] (i < L-1); the adjoint reads psi from
+  // the checkpoints and writes lambda only. Otherwise psi is un-computed in place.
+  float2* ck = (float2*)ckpt_v;
+  const size_t vec = (size_t)batch << P->n;
+  auto out_of = [&](int i) -> float2* { return ck ? ck + (size_t)i * vec : psi; };
   for (int i = 0; i < L - 1; ++i) {
     int flags = F_STORE_PSI | (i == 0 ? F_SYNTH : 0);
-    int rc = launch_pass(P, i, MODE_FWD, flags, batch, theta, x, x_stride, w, psi, psi, nullptr, ws, st);
+    const float2* in = i == 0 ? out_of(0) : out_of(i - 1);
+    int rc = launch_pass(P, i, MODE_FWD, flags, batch, theta, x, x_stride, w, in, out_of(i), nullptr, ws, st);
     if (rc) return rc;
   }
   {
     int flags = (L == 1 ? F_SYNTH : 0) | (L > 1 ? F_STORE_LAM : 0);
-    int rc = launch_pass(P, L - 1, MODE_TURN, flags, batch, theta, x, x_stride, w, psi, psi, lam, ws, st);
+    const float2* in = L > 1 ? out_of(L - 2) : psi;
+    int rc = launch_pass(P, L - 1, MODE_TURN, flags, batch, theta, x, x_stride, w, in, psi, lam, ws, st);
     if (rc) return rc;
     Geometry g = geometry(P, P->passes[L - 1], batch);
     k_reduce_z<<<(batch + 127) / 128, 128, 0, st>>>(ws.zpart, g.cpr, P->n, w, zq, value, batch);
@@ -741,8 +756,9 @@ int lsq_fwd_bwd(const lsq_program* Pc, int batch, const double* theta, const dou
     CUDA_TRY(cudaGetLastError());
   }
   for (int i = L - 2; i >= 0; --i) {
-    int flags = i > 0 ? (F_STORE_PSI | F_STORE_LAM) : 0;
-    int rc = launch_pass(P, i, MODE_BWD, flags, batch, theta, x, x_stride, w, psi, psi, lam, ws, st);
+    int flags = i > 0 ? ((ck ? 0 : F_STORE_PSI) | F_STORE_LAM) : 0;
+    float2* pin = out_of(i);
+    int rc = launch_pass(P, i, MODE_BWD, flags, batch, theta, x, x_stride, w, pin, pin, lam, ws, st);
     if (rc) return rc;
   }
   return finish_grads(P, batch, theta, x, x_stride, ws, grad_rows, grad_sum, egrad_rows, st);

@@ -177,8 +177,11 @@ class Engine:
         free, _ = torch.cuda.mem_get_info(self.device)
         # buffers this engine already holds for a previous call count as available
         held = 0
-        for t in self.__dict__.get("_held_buffers", ()):
-            held += t.numel() * t.element_size()
+        seen = set()
+        for t in self.__dict__.get("_held_buffers") or ():
+            if t is not None and t.data_ptr() not in seen:
+                seen.add(t.data_ptr())
+                held += t.numel() * t.element_size()
         cap = int((free + held) * _STATE_FRACTION) // self.row_bytes(nvec)
         if cap < 1:
             raise CapacityError(
@@ -218,12 +221,29 @@ class Engine:
         return out, zq, val
 
     # -- forward + adjoint ------------------------------------------------------------------------
+    def adjoint_mode(self, batch: int, checkpoint=None) -> str:
+        """'ckpt' (forward checkpoints, adjoint writes lambda only) when every pass output fits
+        for a micro-batch of >= min(batch, 16) rows, else 'recompute' (psi un-computed in place)."""
+        L = len(self.program.passes)
+        if L == 1 or checkpoint is False:
+            return "recompute"
+        if checkpoint is True:
+            return "ckpt"
+        env = os.environ.get("LSQ_ADJOINT")
+        if env in ("ckpt", "recompute"):
+            return env
+        return "ckpt" if self.micro_batch(batch, L) >= min(batch, 16) else "recompute"
+
     def fwd_bwd(self, trainable=None, encoding=None, batch=1, weights=None, rows=True,
-                encoding_grads=True, micro_batch=None, buffers=None):
+                encoding_grads=True, micro_batch=None, buffers=None, checkpoint=None):
         """Forward from |0..0> plus adjoint backward. Returns a dict of CUDA tensors:
         value (B,), zq (B,n), grads (B,T) if rows, grad_sum (T,), encoding_grads (B,E)."""
         th, x, w = self._params(trainable, encoding, weights, batch)
-        mb = micro_batch or self.micro_batch(batch, 2)
+        mode = self.adjoint_mode(batch, checkpoint)
+        L = len(self.program.passes)
+        nvec = L if mode == "ckpt" else 2
+        mb = micro_batch or self.micro_batch(batch, nvec)
+        self.last_micro_batch, self.last_adjoint = mb, mode
         dev = self.device
         f64 = dict(dtype=torch.float64, device=dev)
         value = torch.empty((batch,), **f64)
@@ -232,25 +252,40 @@ class Engine:
         erows = torch.empty((batch, self.E), **f64) if (encoding_grads and self.E) else None
         nchunk = (batch + mb - 1) // mb
         gparts = torch.zeros((nchunk, max(self.T, 1)), **f64)
+        def fits(bufs):
+            return (bufs is not None and bufs[0].shape[0] >= mb
+                    and (mode == "recompute" or (bufs[2] is not None and bufs[2].shape[1] >= mb
+                                                 and bufs[2].shape[0] >= L - 1)))
+
         held = self.__dict__.get("_held_buffers")
-        if buffers is not None and buffers[0].shape[0] >= mb:
-            psi, lam = buffers
-        elif held is not None and held[0].shape[0] >= mb:
-            psi, lam = held
+        if buffers is not None and len(buffers) == 3 and fits(buffers):
+            psi, lam, ck = buffers
+        elif held is not None and fits(held):
+            psi, lam, ck = held
         else:
-            psi = torch.empty((mb, 1 << self.n), dtype=torch.complex64, device=dev)
-            lam = torch.empty_like(psi)
-            self._held_buffers = (psi, lam)
+            self._held_buffers = None
+            lam = torch.empty((mb, 1 << self.n), dtype=torch.complex64, device=dev)
+            if mode == "ckpt":
+                ck = torch.empty((L - 1, mb, 1 << self.n), dtype=torch.complex64, device=dev)
+                psi = lam  # psi is not stored by any pass in checkpoint mode (L > 1)
+            else:
+                ck = None
+                psi = torch.empty_like(lam)
+            self._held_buffers = (psi, lam, ck)
         ws = self.native.workspace(mb)
         lib = _native.lib()
         for c in range(nchunk):
             r0 = c * mb
             b = min(mb, batch - r0)
             xc = x[r0 : r0 + b] if x is not None else None
+            ck_ptr = None
+            if ck is not None:
+                # the checkpoint layout is (L-1) slots of b rows each: compact view for this chunk
+                ck_ptr = ck.data_ptr() if b == ck.shape[1] else ck.view(-1)[: (L - 1) * (b << self.n)].data_ptr()
             _native.check(
-                lib.lsq_fwd_bwd(
+                lib.lsq_fwd_bwd_ckpt(
                     self.native.handle, b, _ptr(th), _ptr(xc), self.E, _ptr(w),
-                    psi.data_ptr(), lam.data_ptr(), zq[r0].data_ptr(), value[r0].data_ptr(),
+                    psi.data_ptr(), lam.data_ptr(), ck_ptr, zq[r0].data_ptr(), value[r0].data_ptr(),
                     grows[r0].data_ptr() if grows is not None else None,
                     gparts[c].data_ptr() if self.T else None,
                     erows[r0].data_ptr() if erows is not None else None,
@@ -261,7 +296,7 @@ class Engine:
                 self.native.profile += [(k, ms, b) for k, ms in self.native.pass_times()]
         gsum = gparts.sum(dim=0)[: self.T] if nchunk > 1 else gparts[0, : self.T]
         return {"value": value, "zq": zq, "grads": grows, "grad_sum": gsum, "encoding_grads": erows,
-                "buffers": (psi, lam)}
+                "buffers": (psi, lam, ck), "adjoint": mode}
 
     def backward_from_state(self, trainable, encoding, final_state, weights=None):
         """Adjoint sweep from a given final state (reference backward_sweep)."""

@@ -37,7 +37,11 @@ import numpy as np
 from .circuits import positions, slot_table, Role
 from .gates import GATE_CODE, GATE_TRAITS, GateKind
 
-COAL = 4  # low physical bits always inside a tile (16 amplitudes = one 128 B line)
+import os as _os
+
+# low physical bits always inside a tile (4 -> 16 amplitudes = one 128 B line); LSQ_COAL
+# overrides it for tiling experiments (profiles/sweep_tiling.sh)
+COAL = int(_os.environ.get("LSQ_COAL", "4"))
 MAX_R = 5  # register bits per thread (2^5 = 32 amplitudes per vector per thread)
 MAX_M_FWD = 14
 MAX_M_BWD = 13

@@ -174,3 +174,19 @@ def test_single_ry_analytic():
         r = gradient(c, np.array([th]))
         assert abs(r.value[0] - np.cos(th)) < 1e-6
         assert abs(r.grads[0, 0] + np.sin(th)) < 1e-6
+
+
+@pytest.mark.parametrize("cfg,n,b", [(2, 14, 5), (5, 13, 3)])
+def test_checkpoint_adjoint_matches_recompute_and_oracle(cfg, n, b):
+    """Forward checkpoints (adjoint writes lambda only) vs in-place un-computation vs oracle."""
+    wl = make_workload(cfg, n=n, batch=b)
+    eng = Engine(wl.circuit)
+    a = eng.fwd_bwd(wl.theta, wl.x, batch=b, weights=wl.weights, checkpoint=True)
+    assert a["adjoint"] == "ckpt"
+    r = eng.fwd_bwd(wl.theta, wl.x, batch=b, weights=wl.weights, checkpoint=False)
+    assert r["adjoint"] == "recompute"
+    ref = orc.gradient(wl.circuit, wl.theta, wl.x, batch=b, weights=wl.weights)
+    for res in (a, r):
+        np.testing.assert_allclose(res["zq"].cpu().numpy(), ref["zq"], atol=Z_TOL)
+        assert_grads_close(res["grads"].cpu().numpy(), ref["grads"])
+        assert_grads_close(res["encoding_grads"].cpu().numpy(), ref["encoding_grads"], "encoding")
