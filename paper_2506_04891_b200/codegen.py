@@ -349,9 +349,37 @@ def _emit_exchange(w, P, a, b, nv):
             w(f"v[{q}][{i}] = s_x[sx{b} ^ {P.soff(b, i)}u];")
 
 
+SMEM_LIMIT = 227 * 1024
+
+
+def generic_smem_bytes(prog, pi: int) -> int:
+    """Mirror of smem_bytes() in csrc/lsq_lib.cu (tables + exchange buffer)."""
+    pp = prog.passes[pi]
+    enc = prog.enc[pi]
+    nt = 1 << (pp.M - pp.R)
+    nw = (nt + 31) // 32
+    nops = sum(len(o) for o in enc["ops"])
+    nsubs = sum(int(op[7]) for ph in enc["ops"] for op in ph if int(op[0]) == S.OP_DRUN)
+    b = 8 * (1 << pp.M)
+    b += 4 * (len(pp.phases) * S.PHASE_WORDS + nops * S.OP_WORDS + nsubs * S.SUB_WORDS + 64)
+    b += 4 * (((enc["matf"] + 3) & ~3) + ((nw * enc["slotf"] + 3) & ~3))
+    b += 8 * 34 + 4 * nw * 32
+    return (b + 15) & ~15
+
+
+def stage_vectors(prog, pi: int, mode: int) -> int:
+    """Vectors prefetched into shared memory by the specialised kernel (0 if they don't fit)."""
+    nv = 1 if mode == MODE_FWD else 2
+    pp = prog.passes[pi]
+    if generic_smem_bytes(prog, pi) + nv * 8 * (1 << pp.M) <= SMEM_LIMIT:
+        return nv
+    return 0
+
+
 def emit_kernel(prog, pi: int, mode: int) -> str:
     P = _Pass(prog, pi)
     nv = 1 if mode == MODE_FWD else 2
+    prefetch = stage_vectors(prog, pi, mode) > 0
     nph = len(P.pp.phases)
     est_regs = 2 * P.NR * nv + 40
     minb = max(1, min(4, 65536 // (P.NT * est_regs)))
@@ -443,10 +471,11 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
                 loc = sum(1 << ph.regs[b] for b in range(P.R) if (i >> b) & 1)
                 w(f"v[{vi}][{i}] = s_stage[{vi * (1 << P.M)} + (tp{k} | {loc}u)];")
 
-    w.block("if (do_load && t0 < t_end)")
-    emit_issue("t0")
-    w.end()
-    w("cp_async_commit();")
+    if prefetch:
+        w.block("if (do_load && t0 < t_end)")
+        emit_issue("t0")
+        w.end()
+        w("cp_async_commit();")
     w.block("for (int t = t0; t < t_end; ++t)")
     tb = [f"((uint64_t)((t >> {j}) & 1)) << {p}" for j, p in enumerate(P.nbit)]
     w(f"const uint64_t tbase = {' | '.join(tb) if tb else '0ull'};")
@@ -458,16 +487,22 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
     w(f"float2 v[{nv}][{P.NR}];")
 
     def emit_load(k):
-        """wait for this tile's prefetch, move it to registers (layout k), prefetch the next"""
+        """wait for this tile's prefetch, move it to registers (layout k), prefetch the next;
+        without a stage (shared memory too small): direct streaming loads in layout k"""
         w.block("if (do_load)")
-        w("cp_async_wait_all();")
-        w("__syncthreads();")
-        emit_stage_read(k)
-        w("__syncthreads();")
-        w.block("if (t + 1 < t_end)")
-        emit_issue("t + 1")
-        w.end()
-        w("cp_async_commit();")
+        if prefetch:
+            w("cp_async_wait_all();")
+            w("__syncthreads();")
+            emit_stage_read(k)
+            w("__syncthreads();")
+            w.block("if (t + 1 < t_end)")
+            emit_issue("t + 1")
+            w.end()
+            w("cp_async_commit();")
+        else:
+            for vi, ptr in ld_vecs:
+                for i in range(P.NR):
+                    w(f"v[{vi}][{i}] = __ldcs({ptr} + base + (gt{k} | {P.goff(k, i)}u));")
         w.end()
 
     def emit_synth(k):
@@ -620,7 +655,8 @@ def generate_kernels(prog) -> list:
         prims = f.read()
     out = []
     for pi, mode in program_modes(prog):
-        out.append((pi, mode, kernel_name(pi, mode), prims + "\n" + emit_kernel(prog, pi, mode) + "\n"))
+        out.append((pi, mode, kernel_name(pi, mode), prims + "\n" + emit_kernel(prog, pi, mode) + "\n",
+                    stage_vectors(prog, pi, mode)))
     return out
 
 

@@ -577,7 +577,8 @@ int jit_compile(const std::string& src, const std::string& cache_dir, std::strin
 }  // namespace
 
 int lsq_program_jit(lsq_program* P, int nk, const char* const* sources, const int* pass_idx,
-                    const int* modes, const char* const* names, const char* cache_dir, int threads) {
+                    const int* modes, const int* stage_vecs, const char* const* names,
+                    const char* cache_dir, int threads) {
   if (!P || nk < 0 || (nk && (!sources || !pass_idx || !modes || !names)))
     return fail(LSQ_EINVAL, "bad JIT arguments");
   std::vector<std::string> cubins(nk), logs(nk);
@@ -607,9 +608,10 @@ int lsq_program_jit(lsq_program* P, int nk, const char* const* sources, const in
     jk.fn = (const void*)kern;
     const PassInfo& pi = P->passes[pass_idx[i]];
     jk.NT = 1 << (pi.M - pi.R);
-    // specialised kernels add a next-tile prefetch stage of NV x 2^M amplitudes
+    // specialised kernels may add a next-tile prefetch stage of stage_vecs[i] x 2^M amplitudes
     const int NV = modes[i] == 0 ? 1 : 2;
-    const size_t sm = smem_bytes(P, pi, NV) + (size_t)NV * sizeof(float2) * ((size_t)1 << pi.M);
+    const int sv = stage_vecs ? stage_vecs[i] : NV;
+    const size_t sm = smem_bytes(P, pi, NV) + (size_t)sv * sizeof(float2) * ((size_t)1 << pi.M);
     CUDA_TRY(cudaFuncSetAttribute(jk.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     jk.smem_set = sm;
   }

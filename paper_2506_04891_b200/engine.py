@@ -72,6 +72,7 @@ class NativeProgram:
         names = (ctypes.c_char_p * n)(*[k[2].encode() for k in ks])
         pidx = (ctypes.c_int * n)(*[k[0] for k in ks])
         modes = (ctypes.c_int * n)(*[k[1] for k in ks])
+        stages = (ctypes.c_int * n)(*[k[4] for k in ks])
         if cache_dir is None:
             cache_dir = os.environ.get("LSQ_CACHE_DIR", os.path.join(os.path.expanduser("~"), ".cache", "lsq_jit"))
         if cache_dir:
@@ -80,7 +81,8 @@ class NativeProgram:
             _native.check(
                 _native.lib().lsq_program_jit(
                     self.handle, n, ctypes.cast(srcs, ctypes.c_void_p), ctypes.cast(pidx, ctypes.c_void_p),
-                    ctypes.cast(modes, ctypes.c_void_p), ctypes.cast(names, ctypes.c_void_p),
+                    ctypes.cast(modes, ctypes.c_void_p), ctypes.cast(stages, ctypes.c_void_p),
+                    ctypes.cast(names, ctypes.c_void_p),
                     cache_dir.encode() if cache_dir else None, 0,
                 )
             )
@@ -124,7 +126,8 @@ class NativeProgram:
 class Engine:
     """A circuit compiled for the device; the object behind the drop-in API."""
 
-    def __init__(self, circuit, M: int | None = None, R: int | None = None, device=None, jit=None):
+    def __init__(self, circuit, M: int | None = None, R: int | None = None, device=None, jit=None,
+                 isolate=()):
         self.device = torch.device(device if device is not None else "cuda")
         if self.device.type != "cuda":
             raise ValueError("the engine runs on CUDA devices only")
@@ -139,7 +142,7 @@ class Engine:
 
             m = min(self.n, M if M is not None else DEFAULT_M)
             R = DEFAULT_R_SPECIALISED if m >= 9 else default_r(m)
-        self.program = compile_circuit(circuit, M=M, R=R)
+        self.program = compile_circuit(circuit, M=M, R=R, isolate=isolate)
         self.native = NativeProgram(self.program, self.device)
         if jit:
             self.native.attach_jit()
@@ -330,7 +333,7 @@ _CACHE: "OrderedDict" = None
 _CACHE_MAX = 8  # engines (programs + held state buffers) kept alive, least recently used evicted
 
 
-def engine_for(circuit, device=None, M=None, R=None, jit=None) -> Engine:
+def engine_for(circuit, device=None, M=None, R=None, jit=None, isolate=()) -> Engine:
     """Cached Engine per (circuit layers, n, tiling, variant, device)."""
     dev = torch.device(device if device is not None else "cuda")
     if dev.type == "cuda" and dev.index is None:
@@ -340,10 +343,11 @@ def engine_for(circuit, device=None, M=None, R=None, jit=None) -> Engine:
         from collections import OrderedDict
 
         _CACHE = OrderedDict()
-    key = (_circuit_key(circuit), M, R, jit, str(dev))
+    isolate = tuple(sorted(set(int(i) for i in isolate)))
+    key = (_circuit_key(circuit), M, R, jit, isolate, str(dev))
     eng = _CACHE.get(key)
     if eng is None:
-        eng = Engine(circuit, M=M, R=R, device=dev, jit=jit)
+        eng = Engine(circuit, M=M, R=R, device=dev, jit=jit, isolate=isolate)
         _CACHE[key] = eng
         while len(_CACHE) > _CACHE_MAX:
             _CACHE.popitem(last=False)

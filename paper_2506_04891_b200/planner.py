@@ -96,6 +96,124 @@ def tiling_of(plan, circuit):
     return getattr(plan, "tile_bits", None), None
 
 
+def layer_signature(layer, n: int) -> tuple:
+    """Layers sharing a signature share one measurement set. Unlike the reference
+    (planner.py:185) the explicit wires are part of it."""
+    role = None if layer.role is None else layer.role.value
+    return (layer.gate.value, layer.pattern.kind.value, tuple(map(tuple, layer.pattern.wires)), n, role)
+
+
+TILE_BITS_CANDIDATES = (10, 11, 12, 13)
+
+
+def _draw(circuit, batch, seed):
+    rng = np.random.default_rng(seed)
+    th = rng.uniform(-np.pi, np.pi, circuit.trainable_count) if circuit.trainable_count else None
+    x = rng.uniform(-np.pi, np.pi, (batch, circuit.encoding_count)) if circuit.encoding_count else None
+    return th, x
+
+
+def time_program(circuit, batch: int, objective: "Objective" = None, M=None, isolate=(), reps: int = 10,
+                 warmup: int = 3, timer=None, seed: int = 0, device=None) -> TimingStats:
+    """Time the whole compiled program (one CUDA variant) with the reference's protocol:
+    `warmup` untimed runs then `reps` timed runs (reference planner.py:106-162). Default clock:
+    CUDA events on the engine's stream; an injected `timer` is called around each rep after
+    a device synchronisation."""
+    import torch
+
+    from .engine import Engine
+
+    objective = objective or Objective.FORWARD
+    if reps < 1:
+        raise ValueError("reps must be at least 1")
+    if warmup < 0:
+        raise ValueError("warmup cannot be negative")
+    eng = Engine(circuit, M=M, isolate=isolate, device=device)
+    th, x = _draw(circuit, batch, seed)
+    th_d = None if th is None else torch.as_tensor(th, device=eng.device)
+    x_d = None if x is None else torch.as_tensor(x, device=eng.device)
+
+    def run():
+        if objective is Objective.FORWARD:
+            eng.forward(th_d, x_d, batch=batch)
+        else:
+            eng.fwd_bwd(th_d, x_d, batch=batch, rows=False, encoding_grads=False)
+
+    for _ in range(warmup):
+        run()
+    samples = np.empty(reps)
+    stream = torch.cuda.current_stream(eng.device)
+    for r in range(reps):
+        if timer is None:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            run()
+            e1.record(stream)
+            e1.synchronize()
+            samples[r] = e0.elapsed_time(e1) / 1e3
+        else:
+            torch.cuda.synchronize(eng.device)
+            t0 = timer()
+            run()
+            torch.cuda.synchronize(eng.device)
+            samples[r] = timer() - t0
+    return TimingStats(float(samples.mean()), float(samples.std()), reps, warmup)
+
+
+def build_plan(circuit, batch: int, objective: "Objective" = None, timer=None, reps: int = 10,
+               warmup: int = 3, seed: int = 0, measure=None, tile_bits=None) -> "Plan":
+    """Per-layer CUDA variant choice by measurement (reference build_plan, planner.py:165-220).
+
+    1. tile exponent M: every candidate (<= n) is timed on the whole program; argmin.
+    2. per layer signature, in order of first appearance: ISOLATED is kept for all layers of the
+       signature iff it measures faster than the current assignment (ties -> FUSED, enum order).
+
+    `measure(layer, kernel) -> TimingStats` replaces real timing (tests): it is asked for the
+    per-layer variants, and `measure(None, M)` for tile exponents.
+    """
+    objective = objective or Objective.FORWARD
+    n = int(circuit.n)
+    layers = list(circuit.layers)
+
+    def timed(M, iso):
+        return time_program(circuit, batch, objective, M=M, isolate=iso, reps=reps, warmup=warmup,
+                            timer=timer, seed=seed)
+
+    if tile_bits is None:
+        cands = sorted({min(n, m) for m in TILE_BITS_CANDIDATES})
+        stats_m = {m: (measure(None, m) if measure is not None else timed(m, ())) for m in cands}
+        tile_bits = min(cands, key=lambda m: (stats_m[m].mean_seconds, -m))
+        base = stats_m[tile_bits]
+    else:
+        base = measure(None, tile_bits) if measure is not None else timed(tile_bits, ())
+    iso: set = set()
+    cache: dict = {}
+    measurements = []
+    assignments = [KernelKind.FUSED] * len(layers)
+    for idx, layer in enumerate(layers):
+        sig = layer_signature(layer, n)
+        if sig not in cache:
+            members = [i for i, l in enumerate(layers) if layer_signature(l, n) == sig]
+            stats = {}
+            if measure is not None:
+                for k in applicable_variants(layer, n):
+                    stats[k] = measure(layer, k)
+            else:
+                stats[KernelKind.FUSED] = base
+                stats[KernelKind.ISOLATED] = timed(tile_bits, sorted(iso | set(members)))
+            best = min(stats, key=lambda k: (stats[k].mean_seconds, kernel_rank(k)))
+            if best is KernelKind.ISOLATED:
+                iso |= set(members)
+                if measure is None:
+                    base = stats[KernelKind.ISOLATED]
+            cache[sig] = (best, stats)
+        best, stats = cache[sig]
+        assignments[idx] = best
+        for k, st in stats.items():
+            measurements.append(PlanMeasurement(idx, k, st.mean_seconds, st.std_seconds, st.reps))
+    return Plan(machine_id(), n, batch, objective, tuple(assignments), tuple(measurements), tile_bits)
+
+
 def machine_id() -> str:
     try:
         import ctypes

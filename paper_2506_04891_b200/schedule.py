@@ -489,22 +489,49 @@ class Program:
         return len(self.passes)
 
 
-def compile_circuit(circuit, M: int | None = None, R: int | None = None) -> Program:
-    """Compile a (reference-compatible) circuit into a pass program."""
+def compile_circuit(circuit, M: int | None = None, R: int | None = None, isolate=()) -> Program:
+    """Compile a (reference-compatible) circuit into a pass program.
+
+    `isolate`: layer indices executed with pass boundaries of their own (planner variant
+    ISOLATED): their gates fuse only among themselves and share no pass with other layers.
+    """
     n = int(circuit.n)
     gates = flatten_gates(circuit)
-    groups = fuse_groups(gates)
-    preds = group_preds(groups)
     if M is None:
         M = min(n, DEFAULT_M)
     M = min(M, n)
-    passes = schedule_passes(groups, n, M)
-    need2 = any(g.arity == 2 and not g.diag for g in groups)
-    for pp in passes:
-        r = default_r(pp.M) if R is None else min(R, pp.M)
-        if need2 and r < 2:
-            r = min(2, pp.M)
-        schedule_phases(pp, groups, preds, n, r)
+    iso = set(int(i) for i in isolate)
+    # segments of consecutive layers: each isolated layer alone, maximal runs of the others
+    segs, cur, cur_key = [], [], None
+    for g in gates:
+        key = ("iso", g.layer) if g.layer in iso else ("run",)
+        if cur and key != cur_key:
+            segs.append(cur)
+            cur = []
+        cur.append(g)
+        cur_key = key
+    if cur or not segs:
+        segs.append(cur)
+    groups, passes = [], []
+    for seg in segs:
+        grp = fuse_groups(seg)
+        preds = group_preds(grp)
+        seg_passes = schedule_passes(grp, n, M) if (grp or not passes) else []
+        need2 = any(g.arity == 2 and not g.diag for g in grp)
+        for pp in seg_passes:
+            r = default_r(pp.M) if R is None else min(R, pp.M)
+            if need2 and r < 2:
+                r = min(2, pp.M)
+            schedule_phases(pp, grp, preds, n, r)
+        off = len(groups)
+        for g in grp:
+            g.gid += off
+        for pp in seg_passes:
+            pp.groups = [x + off for x in pp.groups]
+            for ph in pp.phases:
+                ph.ops = [x + off for x in ph.ops]
+        groups += grp
+        passes += seg_passes
     slot_base, total = {}, 0
     for pp in passes:
         for gid in pp.groups:
@@ -520,6 +547,7 @@ def compile_circuit(circuit, M: int | None = None, R: int | None = None) -> Prog
         c2 = Circuit(circuit.n, circuit.layers)
         T, E = c2.trainable_count, c2.encoding_count
     prog = Program(n, groups, passes, T, E, slot_base, total, M=M, gates=gates)
+    prog.isolate = tuple(sorted(iso))
     encode(prog)
     return prog
 

@@ -190,3 +190,18 @@ def test_checkpoint_adjoint_matches_recompute_and_oracle(cfg, n, b):
         np.testing.assert_allclose(res["zq"].cpu().numpy(), ref["zq"], atol=Z_TOL)
         assert_grads_close(res["grads"].cpu().numpy(), ref["grads"])
         assert_grads_close(res["encoding_grads"].cpu().numpy(), ref["encoding_grads"], "encoding")
+
+
+def test_build_plan_real_timing_and_replay():
+    """Planner over CUDA variants with CUDA-event timing; replaying the plan gives the same
+    results as the default program (reference tests/test_grad.py:119-134 plan independence)."""
+    from paper_2506_04891_b200 import planner as P
+
+    wl = make_workload(4, n=13, batch=4)
+    plan = P.build_plan(wl.circuit, 4, P.Objective.FORWARD_BACKWARD, reps=2, warmup=1)
+    assert plan.tile_bits in (10, 11, 12, 13)
+    assert len(plan.assignments) == len(wl.circuit.layers)
+    a = gradient(wl.circuit, wl.theta, wl.x, batch=4, weights=wl.weights, plan=plan)
+    b = gradient(wl.circuit, wl.theta, wl.x, batch=4, weights=wl.weights)
+    np.testing.assert_allclose(a.zq, b.zq, atol=1e-6)
+    assert_grads_close(a.grads, b.grads)

@@ -65,3 +65,19 @@ def test_program_invariants():
                 if pp.M - pp.R >= S.COAL and i in (0, len(pp.phases) - 1):
                     assert ph.threads[: S.COAL] == list(range(S.COAL))
         assert sorted(seen) == list(range(len(prog.groups)))
+
+
+@pytest.mark.parametrize("cfg", [2, 5])
+def test_isolated_layers_keep_semantics(cfg):
+    """Planner variant ISOLATED (own pass boundaries) must not change results."""
+    wl = make_workload(cfg, n=6, batch=2)
+    iso = [i for i in range(len(wl.circuit.layers)) if i % 3 == 1]
+    prog = S.compile_circuit(wl.circuit, M=4, R=2, isolate=iso)
+    # no pass mixes an isolated layer's groups with other layers
+    for pp in prog.passes:
+        layers = {g.layer for gid in pp.groups for g, _ in prog.groups[gid].gates}
+        if layers & set(iso):
+            assert len(layers) == 1
+    res = Emulator(prog).gradient(wl.theta, wl.x, 2, wl.weights)
+    ref = orc.gradient(wl.circuit, wl.theta, wl.x, batch=2, weights=wl.weights)
+    _cmp(res, ref, atol=1e-8)  # isolated RZ layers become diagonal runs: 2^-32-turn angle grid
