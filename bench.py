@@ -270,13 +270,15 @@ def run_ours(args, world, rank, local):
     theta = torch.as_tensor(wl.theta, device=dev)
     x = torch.as_tensor(wl.x[r0:r1], device=dev)
     w = torch.as_tensor(wl.weights, device=dev)
+    ck = None if args.checkpoint is None else bool(args.checkpoint)
+    # one forward+adjoint step = one CUDA-graph replay of the engine's launch sequence
+    gstep = eng.make_step(b, rows=False, encoding_grads=False, checkpoint=ck,
+                          graph=not args.no_graph)
+    gstep.set_inputs(theta, x, w)
     bufs = None
 
     def step():
-        nonlocal bufs
-        r = eng.fwd_bwd(theta, x, batch=b, weights=w, rows=False, encoding_grads=False,
-                        buffers=bufs, checkpoint=None if args.checkpoint is None else bool(args.checkpoint))
-        bufs = r["buffers"]
+        r = gstep.run()
         if world > 1:
             import torch.distributed as dist
 
@@ -322,7 +324,7 @@ def run_ours(args, world, rank, local):
     for _ in range(nprof):
         eng.native.profile = []
         eng.fwd_bwd(theta, x, batch=b, weights=w, rows=False, encoding_grads=False, micro_batch=mb,
-                    buffers=bufs, checkpoint=None if args.checkpoint is None else bool(args.checkpoint))
+                    checkpoint=ck)
         for kind, t, rows_launch in eng.native.profile:
             mode, pidx = divmod(kind, 1000)
             vec = _pass_vectors(eng.program, mode, pidx, eng.last_adjoint)
@@ -408,6 +410,7 @@ def run_ours(args, world, rank, local):
                    "rows_per_gpu": b, "micro_batch": mb, "adjoint": eng.last_adjoint,
                    "parallelism": f"dp{world}",
                    "passes": len(eng.program.passes), "tile_bits": eng.program.passes[0].M,
+                   "cuda_graph": gstep.graph is not None,
                    "reg_bits": eng.program.passes[0].R, "variant": eng.variant,
                    "l2": f"working set {2 * b * (8 << n) / 2**20:.0f} MiB (psi+lambda) vs 126 MB L2"
                          + (" -> inputs larger than L2" if 2 * b * (8 << n) > 126e6 else " (L2-resident)")},
@@ -436,6 +439,7 @@ def main():
     ap.add_argument("--M", type=int, default=None, help="tile bits per pass (default: planner/engine)")
     ap.add_argument("--R", type=int, default=None, help="register bits per thread")
     ap.add_argument("--batch", type=int, default=None, help="experiments: rows per GPU (not a bench line)")
+    ap.add_argument("--no-graph", action="store_true", help="eager launches instead of a CUDA graph")
     ap.add_argument("--checkpoint", type=int, default=None, choices=[0, 1],
                     help="adjoint with forward checkpoints (1) or in-place un-computation (0); default: engine")
     args = ap.parse_args()

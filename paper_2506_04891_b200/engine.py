@@ -301,6 +301,11 @@ class Engine:
         return {"value": value, "zq": zq, "grads": grows, "grad_sum": gsum, "encoding_grads": erows,
                 "buffers": (psi, lam, ck), "adjoint": mode}
 
+    def make_step(self, batch, rows=True, encoding_grads=True, checkpoint=None, graph=None):
+        """A reusable forward+adjoint step with static device inputs/outputs, replayed as one
+        CUDA graph (the whole launch sequence: tables, passes, reductions, contraction)."""
+        return GradStep(self, batch, rows, encoding_grads, checkpoint, graph)
+
     def backward_from_state(self, trainable, encoding, final_state, weights=None):
         """Adjoint sweep from a given final state (reference backward_sweep)."""
         if not isinstance(final_state, torch.Tensor) or final_state.dtype != torch.complex64:
@@ -327,6 +332,58 @@ class Engine:
         )
         return {"value": value, "zq": zq, "grads": grows[:, : self.T], "grad_sum": gsum[: self.T],
                 "encoding_grads": erows[:, : self.E]}
+
+
+class GradStep:
+    """Static-buffer forward+adjoint step captured in a CUDA graph.
+
+    `run(theta, x, w)` copies new inputs (host or device) into the static buffers and replays
+    the graph; `out` holds the static output tensors (value, zq, grads, grad_sum,
+    encoding_grads). Graphs are disabled with LSQ_GRAPHS=0 (eager replay of the same calls).
+    """
+
+    def __init__(self, eng, batch, rows=True, encoding_grads=True, checkpoint=None, graph=None):
+        self.eng = eng
+        self.batch = int(batch)
+        dev = eng.device
+        f64 = dict(dtype=torch.float64, device=dev)
+        self.theta = torch.zeros((max(eng.T, 1),), **f64)
+        self.x = torch.zeros((self.batch, max(eng.E, 1)), **f64)
+        self.w = torch.ones((eng.n,), **f64)
+        self.kw = dict(batch=self.batch, rows=rows, encoding_grads=encoding_grads, checkpoint=checkpoint)
+        if graph is None:
+            graph = os.environ.get("LSQ_GRAPHS", "1") != "0"
+        self.graph = None
+        self.out = self._call()  # warm-up: JIT, workspace, buffers, micro-batch sizing
+        if graph:
+            torch.cuda.synchronize(dev)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self.out = self._call()
+            self.graph = g
+
+    def _call(self):
+        e = self.eng
+        th = self.theta[: e.T] if e.T else None
+        x = self.x[:, : e.E] if e.E else None
+        return e.fwd_bwd(th, x, weights=self.w, **self.kw)
+
+    def set_inputs(self, theta=None, x=None, w=None):
+        e = self.eng
+        if theta is not None and e.T:
+            self.theta[: e.T].copy_(torch.as_tensor(np.asarray(theta, dtype=np.float64)) if not isinstance(theta, torch.Tensor) else theta)
+        if x is not None and e.E:
+            self.x[:, : e.E].copy_(torch.as_tensor(np.asarray(x, dtype=np.float64)) if not isinstance(x, torch.Tensor) else x)
+        if w is not None:
+            self.w.copy_(torch.as_tensor(np.asarray(w, dtype=np.float64)) if not isinstance(w, torch.Tensor) else w)
+
+    def run(self, theta=None, x=None, w=None):
+        self.set_inputs(theta, x, w)
+        if self.graph is not None:
+            self.graph.replay()
+        else:
+            self.out = self._call()
+        return self.out
 
 
 _CACHE: "OrderedDict" = None

@@ -47,7 +47,14 @@ def gradient(circuit, trainable=None, encoding=None, batch: int = 1, plan=None, 
     if batch < 1:
         raise ValueError(f"batch must be positive, got {batch}")
     eng = _engine(circuit, plan, device)
-    r = eng.fwd_bwd(trainable, encoding, batch=batch, weights=weights)
+    # one captured CUDA graph per (batch, weighted) and engine: inputs copied in, graph replayed
+    key = ("grad_step", batch, weights is None)
+    steps = eng.__dict__.setdefault("_steps", {})
+    step = steps.get(key)
+    if step is None:
+        steps.clear()  # keep one step's static buffers alive per engine
+        step = steps[key] = eng.make_step(batch)
+    r = step.run(trainable, encoding, np.ones(circuit.n) if weights is None else weights)
     T, E = eng.T, eng.E
     return GradResult(
         value=_np(r["value"], (batch,)),
