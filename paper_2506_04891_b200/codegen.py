@@ -397,7 +397,10 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
     w("float* s_zw = reinterpret_cast<float*>(s_z + 34);  // [NW][32] per-warp <Z> partials")
     # next-tile prefetch stage [NV][2^M], natural local order, after the fixed tables so the
     # generic kernel's shared-memory size plus NV x 2^M x 8 B covers it (lsq_program_jit)
+    use_prefix = bool(getattr(prog, "prefix", None)) and pi == 0
     w(f"float2* s_stage = reinterpret_cast<float2*>((reinterpret_cast<size_t>(s_zw + {P.NW * 32}) + 15) & ~(size_t)15);")
+    # the prefix vectors live in the first 8*n bytes of the exchange buffer's tail region: use a
+    # dedicated register-free path -- they are read from global (L1-cached, 16 B per wire)
     w("const int tid = threadIdx.x, warp = tid >> 5;")
     w("const int row = blockIdx.x / A.ctas_per_row, cslot = blockIdx.x % A.ctas_per_row;")
     w("const int mode = A.mode, flags = A.flags;")
@@ -505,9 +508,107 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
                     w(f"v[{vi}][{i}] = __ldcs({ptr} + base + (gt{k} | {P.goff(k, i)}u));")
         w.end()
 
+    def wire_of_local(lb):
+        return P.n - 1 - P.pbit[lb]
+
+    def pv(wire, idx_expr):
+        """prefix vector entry v_wire[idx] (float2) of this CTA's row"""
+        return f"reinterpret_cast<const float2*>(A.ptab)[((size_t)row * {P.n} + {wire}) * 2 + ({idx_expr})]"
+
     def emit_synth(k):
+        if not use_prefix:
+            for i in range(P.NR):
+                w(f"v[0][{i}] = make_float2(((tbase | (uint64_t)(gt{k} | {P.goff(k, i)}u)) == 0) ? 1.f : 0.f, 0.f);")
+            return
+        # product state (x)_w v_w: constant factor over thread and tile bits, then a Kronecker
+        # expansion over the register bits (one complex multiply per amplitude)
+        ph = P.pp.phases[k]
+        w("{")
+        w.ind += 1
+        w("float2 cst = make_float2(1.f, 0.f);")
+        for lb in ph.threads:
+            w(f"{{ const float2 f_ = {pv(wire_of_local(lb), f'(tp{k} >> {lb}) & 1u')}; cst = cm(f_.x, f_.y, cst); }}")
+        for p in P.nbit:
+            w(f"{{ const float2 f_ = {pv(P.n - 1 - p, f'(int)((tbase >> {p}) & 1ull)')}; cst = cm(f_.x, f_.y, cst); }}")
+        w("v[0][0] = cst;")
+        for kk in range(P.R):
+            wr = wire_of_local(ph.regs[kk])
+            w(f"{{ const float2 a0 = {pv(wr, '0')}, a1 = {pv(wr, '1')};")
+            for i in range(1 << kk):
+                w(f"  v[0][{i | (1 << kk)}] = cm(a1.x, a1.y, v[0][{i}]); v[0][{i}] = cm(a0.x, a0.y, v[0][{i}]);")
+            w("}")
+        w.ind -= 1
+        w("}")
+
+    def emit_prefix_lambda(k):
+        """Lambda_w(a) = sum_{j: bit_w(j)=a} conj(lam_j) prod_{w' != w} v_w'(bit_w'(j)) for every
+        prefix wire with a coupling slot, at the prefix boundary (end of the last adjoint pass)."""
+        slots = {}
+        pre = prog.prefix
+        for wire, gid in pre.items():
+            sl = prog.enc[0]["prefix_slots"].get(gid)
+            if sl is not None:
+                slots[wire] = sl
+        if not slots:
+            return
+        ph = P.pp.phases[k]
+        reg_w = [wire_of_local(ph.regs[kk]) for kk in range(P.R)]
+        consts = [(wire_of_local(lb), f"(tp{k} >> {lb}) & 1u") for lb in ph.threads]
+        consts += [(P.n - 1 - p, f"(int)((tbase >> {p}) & 1ull)") for p in P.nbit]
+        w("{")
+        w.ind += 1
+        # constant factors, prefix / suffix products for leave-one-out
+        nc = len(consts)
+        for ci, (wr, ix) in enumerate(consts):
+            w(f"const float2 f{ci} = {pv(wr, ix)};")
+        w("float2 pre0 = make_float2(1.f, 0.f);")
+        for ci in range(nc):
+            w(f"const float2 pre{ci + 1} = cm(f{ci}.x, f{ci}.y, pre{ci});")
+        w(f"const float2 suf{nc} = make_float2(1.f, 0.f);")
+        for ci in range(nc - 1, -1, -1):
+            w(f"const float2 suf{ci} = cm(f{ci}.x, f{ci}.y, suf{ci + 1});")
+        # register Kronecker product Kr and S = sum conj(lam) Kr
+        w(f"float2 kr[{P.NR}]; kr[0] = make_float2(1.f, 0.f);")
+        for kk in range(P.R):
+            w(f"{{ const float2 a0 = {pv(reg_w[kk], '0')}, a1 = {pv(reg_w[kk], '1')};")
+            for i in range(1 << kk):
+                w(f"  kr[{i | (1 << kk)}] = cm(a1.x, a1.y, kr[{i}]); kr[{i}] = cm(a0.x, a0.y, kr[{i}]);")
+            w("}")
+        w("float2 S_ = make_float2(0.f, 0.f);")
         for i in range(P.NR):
-            w(f"v[0][{i}] = make_float2(((tbase | (uint64_t)(gt{k} | {P.goff(k, i)}u)) == 0) ? 1.f : 0.f, 0.f);")
+            w(f"S_ = cjfma(v[1][{i}], kr[{i}], S_);")
+        # constant-factor wires: Lambda_t(b_t) += C_{not t} * S
+        for ci, (wr, ix) in enumerate(consts):
+            if wr not in slots:
+                continue
+            w(f"{{ const float2 cn = cm(suf{ci + 1}.x, suf{ci + 1}.y, pre{ci}); const float2 val = cm(cn.x, cn.y, S_);")
+            w(f"  const int b_ = {ix}; float acc[4] = {{b_ ? 0.f : val.x, b_ ? 0.f : val.y, b_ ? val.x : 0.f, b_ ? val.y : 0.f}};")
+            w(f"  warp_accumulate<NT, 4>(acc, wacc + {slots[wr]}); }}")
+        # register wires: Lambda_k(a) = C_all * sum_{b_k(i)=a} conj(lam_i) prod_{k' != k} v_k'(b_k'(i))
+        for kk in range(P.R):
+            wr = reg_w[kk]
+            if wr not in slots:
+                continue
+            others = [k2 for k2 in range(P.R) if k2 != kk]
+            w("{")
+            w.ind += 1
+            w(f"float2 ko[{1 << (P.R - 1)}]; ko[0] = pre{nc};")
+            for t2, k2 in enumerate(others):
+                w(f"{{ const float2 a0 = {pv(reg_w[k2], '0')}, a1 = {pv(reg_w[k2], '1')};")
+                for i in range(1 << t2):
+                    w(f"  ko[{i | (1 << t2)}] = cm(a1.x, a1.y, ko[{i}]); ko[{i}] = cm(a0.x, a0.y, ko[{i}]);")
+                w("}")
+            w("float2 L0 = make_float2(0.f, 0.f), L1 = make_float2(0.f, 0.f);")
+            for i in range(P.NR):
+                # index into ko: bits of i without bit kk, in the order of `others`
+                oi = sum(((i >> k2) & 1) << t2 for t2, k2 in enumerate(others))
+                tgt = "L1" if (i >> kk) & 1 else "L0"
+                w(f"{tgt} = cjfma(v[1][{i}], ko[{oi}], {tgt});")
+            w(f"float acc[4] = {{L0.x, L0.y, L1.x, L1.y}}; warp_accumulate<NT, 4>(acc, wacc + {slots[wr]});")
+            w.ind -= 1
+            w("}")
+        w.ind -= 1
+        w("}")
 
     def emit_fwd_phases():
         for k in range(nph):
@@ -598,6 +699,8 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
     elif mode == MODE_BWD:
         emit_load(last)
         emit_bwd_phases()
+        if use_prefix:
+            emit_prefix_lambda(0)
         emit_store(0, "psi")
         emit_store(0, "lam")
     else:
@@ -617,6 +720,8 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
         emit_zpart(last)
         emit_lambda_init(last)
         emit_bwd_phases()
+        if use_prefix and len(prog.passes) == 1:
+            emit_prefix_lambda(0)
         emit_store(0, "psi")
         emit_store(0, "lam")
     w.end()  # tile loop

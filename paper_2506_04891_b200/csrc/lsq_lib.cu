@@ -67,6 +67,28 @@ __global__ void k_row_table(const int* W, const double* fvals, const double* the
   }
 }
 
+// product-state prefix vectors: ptab[row][w] = U_w |0> (column 0 of the wire's prefix group),
+// |0> for wires without one
+__global__ void k_prefix_table(const int* W, const double* fvals, const double* theta, const double* x,
+                               int x_stride, int batch, float* ptab) {
+  const int n = W[2];
+  const int64_t total = (int64_t)batch * n;
+  const int* pre = W + sec_off(W, SEC_PREFIX);
+  for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total;
+       id += (int64_t)gridDim.x * blockDim.x) {
+    const int b = (int)(id / n), w = (int)(id % n);
+    float* o = ptab + id * 4;
+    const int gid = pre[w * 4];
+    if (gid < 0) {
+      o[0] = 1.f; o[1] = 0.f; o[2] = 0.f; o[3] = 0.f;
+      continue;
+    }
+    cd U[16];
+    group_unitary(W, gid, fvals, theta, x ? x + (size_t)b * x_stride : nullptr, U);
+    o[0] = (float)U[0].r; o[1] = (float)U[0].i; o[2] = (float)U[2].r; o[3] = (float)U[2].i;
+  }
+}
+
 // Macc[b][first + f] = sum_c part[(b*cpr + c)*slotf + f]   (fixed order)
 __global__ void k_reduce_part(const double* part, int cpr, int slotf, double* macc, int slot_total,
                               int first, int batch) {
@@ -115,7 +137,14 @@ __global__ void k_contract(const int* W, const double* fvals, const double* thet
     const double* mrow = macc + (size_t)b * slot_total + grp[GW_SLOT];
     cd Mm[16];
     mat_zero(Mm, d);
-    if (grp[GW_DIAG]) {
+    if (grp[GW_PREFIX]) {
+      // prefix group at the prefix boundary: M_ab = Lambda(a) v(b), v = U|0>
+      cd U0[16];
+      group_unitary(W, gid, fvals, theta, xrow, U0);
+      const cd v[2] = {U0[0], U0[2]};
+      for (int a = 0; a < 2; ++a)
+        for (int bb = 0; bb < 2; ++bb) Mm[a * 2 + bb] = cmulx(cd{mrow[2 * a], mrow[2 * a + 1]}, v[bb]);
+    } else if (grp[GW_DIAG]) {
       for (int e = 0; e < d; ++e) Mm[e * d + e] = cd{mrow[2 * e], mrow[2 * e + 1]};
     } else {
       for (int e = 0; e < d * d; ++e) Mm[e] = cd{mrow[2 * e], mrow[2 * e + 1]};
@@ -227,7 +256,7 @@ struct JitKernel {
 struct lsq_program {
   std::vector<JitKernel> jit;  // [pass * 3 + mode], fn == nullptr -> generic kernel
   std::vector<cudaLibrary_t> jit_libs;
-  int n, T, E, npasses, ngroups, slot_total, nperrow;
+  int n, T, E, npasses, ngroups, slot_total, nperrow, prefix = 0;
   int* d_words = nullptr;
   double* d_fvals = nullptr;
   std::vector<int> words;
@@ -286,6 +315,7 @@ Geometry geometry(const lsq_program* P, const PassInfo& pi, int batch) {
 struct WS {
   float* gmats;
   float* rowtab;
+  float* ptab;
   double* part;
   double* zpart;
   double* macc;
@@ -310,6 +340,7 @@ WS carve(const lsq_program* P, int batch, void* base) {
   }
   size_t o_g = take(sizeof(float) * 32 * (size_t)std::max(P->ngroups, 1));
   size_t o_r = take(sizeof(float) * 32 * (size_t)batch * std::max(P->nperrow, 1));
+  size_t o_pt = take(sizeof(float) * 4 * (size_t)batch * (P->prefix ? P->n : 1));
   size_t o_p = take(sizeof(double) * std::max(maxpart, (size_t)1));
   size_t o_z = take(sizeof(double) * std::max(maxz, (size_t)1));
   size_t o_m = take(sizeof(double) * (size_t)batch * std::max(P->slot_total, 1));
@@ -320,6 +351,7 @@ WS carve(const lsq_program* P, int batch, void* base) {
     char* c = (char*)base;
     w.gmats = (float*)(c + o_g);
     w.rowtab = (float*)(c + o_r);
+    w.ptab = (float*)(c + o_pt);
     w.part = (double*)(c + o_p);
     w.zpart = (double*)(c + o_z);
     w.macc = (double*)(c + o_m);
@@ -336,6 +368,8 @@ int launch_pass(lsq_program* P, int pi_idx, int mode, int flags, int batch, cons
   const int NV = mode == MODE_FWD ? 1 : 2;
   const KEntry& k = NV == 1 ? pi.k1 : pi.k2;
   const bool have_jit = !P->jit.empty() && P->jit[pi_idx * 3 + mode].fn;
+  if (P->prefix && !have_jit)
+    return fail(LSQ_EPLAN, "programs with a synthesized product-state prefix need the specialised kernels");
   if (!k.fn && !have_jit)
     return fail(LSQ_EPLAN, "no kernel for pass " + std::to_string(pi_idx) + " (M=" + std::to_string(pi.M) +
                                ", R=" + std::to_string(pi.R) + "): attach the specialised kernels");
@@ -355,6 +389,7 @@ int launch_pass(lsq_program* P, int pi_idx, int mode, int flags, int batch, cons
   A.gmats = ws.gmats;
   A.rowtab = ws.rowtab;
   A.nperrow = P->nperrow;
+  A.ptab = ws.ptab;
   A.theta = theta;
   A.x = x;
   A.x_stride = x_stride;
@@ -457,11 +492,12 @@ int lsq_program_create(const int32_t* words, int64_t n_words, const double* fval
   P->npasses = W[6];
   P->ngroups = W[7];
   P->nperrow = W[HDR_NPERROW];
+  P->prefix = W[HDR_PREFIX];
   if (P->n < 1 || P->n > 30) {
     delete P;
     return fail(LSQ_EINVAL, "n out of range (1..30)");
   }
-  for (int s = 0; s < 7; ++s) {
+  for (int s = 0; s < N_SECTIONS; ++s) {
     if (sec_off(W, s) < HDR_WORDS || sec_off(W, s) > n_words) {
       delete P;
       return fail(LSQ_EINVAL, "corrupt program section table");
@@ -679,6 +715,11 @@ int lsq_forward(const lsq_program* Pc, int batch, const double* theta, const dou
     k_row_table<<<(int)std::min<int64_t>((tot + 127) / 128, 8192), 128, 0, st>>>(P->d_words, P->d_fvals, theta, x, x_stride, batch, ws.rowtab);
     P->launches++;
   }
+  if (P->prefix) {
+    const int64_t tot = (int64_t)batch * P->n;
+    k_prefix_table<<<(int)std::min<int64_t>((tot + 127) / 128, 8192), 128, 0, st>>>(P->d_words, P->d_fvals, theta, x, x_stride, batch, ws.ptab);
+    P->launches++;
+  }
   CUDA_TRY(cudaGetLastError());
   const float2* src = (const float2*)psi_in;
   float2* dst = (float2*)psi_out;
@@ -729,6 +770,11 @@ int lsq_fwd_bwd_ckpt(const lsq_program* Pc, int batch, const double* theta, cons
   if (P->nperrow && x) {
     const int64_t tot = (int64_t)batch * P->ngroups;
     k_row_table<<<(int)std::min<int64_t>((tot + 127) / 128, 8192), 128, 0, st>>>(P->d_words, P->d_fvals, theta, x, x_stride, batch, ws.rowtab);
+    P->launches++;
+  }
+  if (P->prefix) {
+    const int64_t tot = (int64_t)batch * P->n;
+    k_prefix_table<<<(int)std::min<int64_t>((tot + 127) / 128, 8192), 128, 0, st>>>(P->d_words, P->d_fvals, theta, x, x_stride, batch, ws.ptab);
     P->launches++;
   }
   CUDA_TRY(cudaGetLastError());
@@ -788,6 +834,11 @@ int lsq_bwd_from_state(const lsq_program* Pc, int batch, const double* theta, co
   if (P->nperrow && x) {
     const int64_t tot = (int64_t)batch * P->ngroups;
     k_row_table<<<(int)std::min<int64_t>((tot + 127) / 128, 8192), 128, 0, st>>>(P->d_words, P->d_fvals, theta, x, x_stride, batch, ws.rowtab);
+    P->launches++;
+  }
+  if (P->prefix) {
+    const int64_t tot = (int64_t)batch * P->n;
+    k_prefix_table<<<(int)std::min<int64_t>((tot + 127) / 128, 8192), 128, 0, st>>>(P->d_words, P->d_fvals, theta, x, x_stride, batch, ws.ptab);
     P->launches++;
   }
   CUDA_TRY(cudaGetLastError());

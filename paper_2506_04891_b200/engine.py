@@ -127,7 +127,7 @@ class Engine:
     """A circuit compiled for the device; the object behind the drop-in API."""
 
     def __init__(self, circuit, M: int | None = None, R: int | None = None, device=None, jit=None,
-                 isolate=()):
+                 isolate=(), prefix=None):
         self.device = torch.device(device if device is not None else "cuda")
         if self.device.type != "cuda":
             raise ValueError("the engine runs on CUDA devices only")
@@ -142,7 +142,12 @@ class Engine:
 
             m = min(self.n, M if M is not None else DEFAULT_M)
             R = DEFAULT_R_SPECIALISED if m >= 9 else default_r(m)
-        self.program = compile_circuit(circuit, M=M, R=R, isolate=isolate)
+        if prefix is None:
+            prefix = jit and os.environ.get("LSQ_PREFIX", "1") != "0"
+        if prefix and not jit:
+            raise ValueError("the product-state prefix needs the specialised (JIT) kernels")
+        self.program = compile_circuit(circuit, M=M, R=R, isolate=isolate, prefix=prefix)
+        self.prefix = bool(self.program.prefix)
         self.native = NativeProgram(self.program, self.device)
         if jit:
             self.native.attach_jit()
@@ -198,6 +203,9 @@ class Engine:
         """Evolve `state` ((B, 2^n) complex64 CUDA tensor, or None = |0..0> with `batch` rows)
         through the circuit into a NEW tensor. Returns (psi, zq, value)."""
         if state is not None:
+            if self.prefix:
+                raise ValueError("this program synthesizes its |0..0> prefix; compile with prefix=False "
+                                 "to evolve an arbitrary input state")
             if not isinstance(state, torch.Tensor) or state.dtype != torch.complex64:
                 raise ValueError("state must be a complex64 torch tensor")
             if state.device != self.device:
@@ -308,6 +316,8 @@ class Engine:
 
     def backward_from_state(self, trainable, encoding, final_state, weights=None):
         """Adjoint sweep from a given final state (reference backward_sweep)."""
+        if self.prefix:
+            raise ValueError("backward_from_state needs a program compiled with prefix=False")
         if not isinstance(final_state, torch.Tensor) or final_state.dtype != torch.complex64:
             raise ValueError("final state must be a complex64 torch tensor")
         final_state = final_state.to(self.device).contiguous()
@@ -390,7 +400,7 @@ _CACHE: "OrderedDict" = None
 _CACHE_MAX = 8  # engines (programs + held state buffers) kept alive, least recently used evicted
 
 
-def engine_for(circuit, device=None, M=None, R=None, jit=None, isolate=()) -> Engine:
+def engine_for(circuit, device=None, M=None, R=None, jit=None, isolate=(), prefix=None) -> Engine:
     """Cached Engine per (circuit layers, n, tiling, variant, device)."""
     dev = torch.device(device if device is not None else "cuda")
     if dev.type == "cuda" and dev.index is None:
@@ -401,10 +411,10 @@ def engine_for(circuit, device=None, M=None, R=None, jit=None, isolate=()) -> En
 
         _CACHE = OrderedDict()
     isolate = tuple(sorted(set(int(i) for i in isolate)))
-    key = (_circuit_key(circuit), M, R, jit, isolate, str(dev))
+    key = (_circuit_key(circuit), M, R, jit, isolate, prefix, str(dev))
     eng = _CACHE.get(key)
     if eng is None:
-        eng = Engine(circuit, M=M, R=R, device=dev, jit=jit, isolate=isolate)
+        eng = Engine(circuit, M=M, R=R, device=dev, jit=jit, isolate=isolate, prefix=prefix)
         _CACHE[key] = eng
         while len(_CACHE) > _CACHE_MAX:
             _CACHE.popitem(last=False)

@@ -71,7 +71,7 @@ def backward_sweep(circuit, trainable=None, encoding=None, final_state: StateBat
     if final_state is None:
         raise ValueError("backward_sweep needs the forward-pass final state")
     trainable, encoding = check_parameters(circuit, trainable, encoding, final_state.batch)
-    eng = _engine(circuit, plan, final_state.amplitudes.device)
+    eng = _engine(circuit, plan, final_state.amplitudes.device, prefix=False)
     r = eng.backward_from_state(trainable, encoding, final_state.amplitudes, weights=weights)
     b = final_state.batch
     return GradResult(

@@ -137,6 +137,7 @@ class Group:
     gid: int
     wires: tuple  # group basis order (first wire = more significant local bit)
     gates: list = field(default_factory=list)  # list of (GateRef, reversed: bool)
+    prefix: bool = False  # synthesized product-state prefix (not executed by any pass)
 
     @property
     def arity(self) -> int:
@@ -178,6 +179,8 @@ class Group:
     def slot_floats(self) -> int:
         if not self.needs_grad:
             return 0
+        if self.prefix:
+            return 4  # Lambda(0), Lambda(1): M_ab = Lambda(a) v(b), v = U|0>
         if self.diag:
             return 2 << self.arity  # complex diagonal of M
         return 8 if self.arity == 1 else 32
@@ -327,12 +330,14 @@ def _greedy_pass(order, groups, preds, done, base, M, first_forced=None):
     return S, chosen, work
 
 
-def schedule_passes(groups, n, M, seeds: int = 12) -> list[PassPlan]:
+def schedule_passes(groups, n, M, seeds: int = 12, skip=()) -> list[PassPlan]:
     """Greedy tile-pass partition; tries a few seeds per pass and keeps the one that
-    schedules the most non-diagonal work."""
+    schedules the most non-diagonal work. Groups in `skip` (the synthesized product-state
+    prefix) count as already executed."""
     preds = group_preds(groups)
-    remaining = [g.gid for g in groups]
-    done: set = set()
+    skip = set(skip)
+    remaining = [g.gid for g in groups if g.gid not in skip]
+    done: set = set(skip)
     passes = []
     if n <= M:
         return [PassPlan(set(range(n)), remaining, M=n)]
@@ -489,7 +494,19 @@ class Program:
         return len(self.passes)
 
 
-def compile_circuit(circuit, M: int | None = None, R: int | None = None, isolate=()) -> Program:
+def prefix_groups(groups) -> dict:
+    """wire -> gid of its product-state prefix group: the FIRST group touching the wire when it
+    is a single-qubit group. Applied to |0..0> these groups give the product state
+    (x)_w U_w|0>, which the first pass synthesizes instead of executing them."""
+    first: dict = {}
+    for g in groups:
+        for w in g.wires:
+            first.setdefault(w, g)
+    return {w: g.gid for w, g in first.items() if g.arity == 1}
+
+
+def compile_circuit(circuit, M: int | None = None, R: int | None = None, isolate=(),
+                    prefix: bool = False) -> Program:
     """Compile a (reference-compatible) circuit into a pass program.
 
     `isolate`: layer indices executed with pass boundaries of their own (planner variant
@@ -513,10 +530,15 @@ def compile_circuit(circuit, M: int | None = None, R: int | None = None, isolate
     if cur or not segs:
         segs.append(cur)
     groups, passes = [], []
-    for seg in segs:
+    pre: dict = {}
+    for si, seg in enumerate(segs):
         grp = fuse_groups(seg)
         preds = group_preds(grp)
-        seg_passes = schedule_passes(grp, n, M) if (grp or not passes) else []
+        skip = ()
+        if prefix and si == 0:
+            pre = prefix_groups(grp)
+            skip = set(pre.values())
+        seg_passes = schedule_passes(grp, n, M, skip=skip) if (grp or not passes) else []
         need2 = any(g.arity == 2 and not g.diag for g in grp)
         for pp in seg_passes:
             r = default_r(pp.M) if R is None else min(R, pp.M)
@@ -532,9 +554,14 @@ def compile_circuit(circuit, M: int | None = None, R: int | None = None, isolate
                 ph.ops = [x + off for x in ph.ops]
         groups += grp
         passes += seg_passes
+    for w, gid in pre.items():
+        groups[gid].prefix = True
+    if passes:
+        # the prefix groups' couplings are produced by the last adjoint pass (pass 0)
+        passes[0].prefix_groups = [gid for w, gid in sorted(pre.items())]
     slot_base, total = {}, 0
     for pp in passes:
-        for gid in pp.groups:
+        for gid in pp.groups + getattr(pp, "prefix_groups", []):
             g = groups[gid]
             if g.slot_floats:
                 slot_base[gid] = total
@@ -548,6 +575,7 @@ def compile_circuit(circuit, M: int | None = None, R: int | None = None, isolate
         T, E = c2.trainable_count, c2.encoding_count
     prog = Program(n, groups, passes, T, E, slot_base, total, M=M, gates=gates)
     prog.isolate = tuple(sorted(iso))
+    prog.prefix = {w: gid for w, gid in pre.items()}
     encode(prog)
     return prog
 
@@ -577,7 +605,7 @@ def encode(prog: Program) -> None:
         group_w.append(
             [g.arity, int(g.diag), int(g.perrow), len(g.gates), g0, wa, wb,
              prog.slot_base.get(g.gid, -1), g.slot_floats, g.mat_floats, int(g.needs_grad),
-             rowidx if g.perrow else -1, 0, 0, 0, 0]
+             rowidx if g.perrow else -1, int(g.prefix), 0, 0, 0]
         )
         rowidx += int(g.perrow)
     pass_w, phase_w, op_w, sub_w, pgrp_w = [], [], [], [], []
@@ -599,6 +627,11 @@ def encode(prog: Program) -> None:
             if g.slot_floats:
                 slot_off[gid] = so
                 so += g.slot_floats
+        for gid in getattr(pp, "prefix_groups", []):
+            g = prog.groups[gid]
+            if g.slot_floats:
+                slot_off[gid] = so
+                so += g.slot_floats
         pg0 = len(pgrp_w)
         for gid in pp.groups:
             pgrp_w.append([gid, mat_off[gid], slot_off.get(gid, -1), 0])
@@ -606,9 +639,12 @@ def encode(prog: Program) -> None:
         for p in pp.phys_of_local:
             tile_mask |= 1 << p
         ph0 = len(phase_w)
-        first_slot = min((prog.slot_base[g] for g in pp.groups if g in prog.slot_base), default=0)
+        first_slot = min((prog.slot_base[g] for g in pp.groups + getattr(pp, "prefix_groups", [])
+                          if g in prog.slot_base), default=0)
         enc = {"ops": [], "subs": sub_w, "matf": mo, "slotf": so,
-               "pgroups": [(gid, mat_off[gid]) for gid in pp.groups]}
+               "pgroups": [(gid, mat_off[gid]) for gid in pp.groups],
+               "prefix_slots": {gid: slot_off[gid] for gid in getattr(pp, "prefix_groups", [])
+                                if gid in slot_off}}
         prog.enc.append(enc)
         for ph in pp.phases:
             op0 = len(op_w)
@@ -670,9 +706,14 @@ def encode(prog: Program) -> None:
              first_slot, ops_lo, len(op_w) - ops_lo, subs_lo, len(sub_w) - subs_lo]
             + [0] * (PASS_WORDS - 14)
         )
+    # prefix section: per wire, the pass-0 slot offset of its prefix group's Lambda (-1: none or
+    # no gradient needed) and its gid (-1: no prefix group, the factor is |0>)
+    pre = getattr(prog, "prefix", {}) or {}
+    pslots = prog.enc[0]["prefix_slots"] if prog.enc else {}
+    prefix_w = [[pre.get(w, -1), pslots.get(pre.get(w, -1), -1), 0, 0] for w in range(n)] if pre else []
     hdr = [0] * HDR_WORDS
-    sections = [gates_w, group_w, pass_w, phase_w, op_w, sub_w, pgrp_w]
-    widths = [GATE_WORDS, GROUP_WORDS, PASS_WORDS, PHASE_WORDS, OP_WORDS, SUB_WORDS, 4]
+    sections = [gates_w, group_w, pass_w, phase_w, op_w, sub_w, pgrp_w, prefix_w]
+    widths = [GATE_WORDS, GROUP_WORDS, PASS_WORDS, PHASE_WORDS, OP_WORDS, SUB_WORDS, 4, 4]
     hdr[0] = MAGIC
     hdr[1] = 1
     hdr[2] = n
@@ -681,7 +722,8 @@ def encode(prog: Program) -> None:
     hdr[5] = prog.slot_total
     hdr[6] = len(prog.passes)
     hdr[7] = len(prog.groups)
-    hdr[22] = rowidx  # number of per-row (encoding) groups
+    hdr[24] = rowidx  # number of per-row (encoding) groups
+    hdr[25] = int(bool(pre))  # product-state prefix synthesized by the first pass
     off = HDR_WORDS
     flat = []
     for si, (sec, wd) in enumerate(zip(sections, widths)):
@@ -702,8 +744,8 @@ def section(words: np.ndarray, idx: int, width: int) -> np.ndarray:
     return words[off : off + cnt * width].reshape(cnt, width)
 
 
-SEC_GATES, SEC_GROUPS, SEC_PASSES, SEC_PHASES, SEC_OPS, SEC_SUBS, SEC_PGROUPS = range(7)
-SEC_WIDTH = [GATE_WORDS, GROUP_WORDS, PASS_WORDS, PHASE_WORDS, OP_WORDS, SUB_WORDS, 4]
+SEC_GATES, SEC_GROUPS, SEC_PASSES, SEC_PHASES, SEC_OPS, SEC_SUBS, SEC_PGROUPS, SEC_PREFIX = range(8)
+SEC_WIDTH = [GATE_WORDS, GROUP_WORDS, PASS_WORDS, PHASE_WORDS, OP_WORDS, SUB_WORDS, 4, 4]
 
 
 def describe(prog: Program) -> str:

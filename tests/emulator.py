@@ -289,14 +289,57 @@ class Emulator:
         if Lm is not None:
             lam[:, idx] = Lm
 
+    # -- product-state prefix ----------------------------------------------------------------
+    def prefix_vectors(self, theta, x, batch):
+        """v[b, w] = U_w |0> for wires with a prefix group, |0> otherwise (B, n, 2)."""
+        v = np.zeros((batch, self.n, 2), dtype=complex)
+        v[:, :, 0] = 1
+        pre = S.section(self.w, S.SEC_PREFIX, 4) if int(self.w[25]) else []
+        for w, row in enumerate(pre):
+            gid = int(row[0])
+            if gid >= 0:
+                U = group_unitary(self.w, self.fv, theta, x, gid)
+                v[:, w, :] = U[..., :, 0] if U.ndim == 3 else U[None, :, 0]
+        return v
+
+    def product_state(self, v, skip=None):
+        B = v.shape[0]
+        out = np.ones((B, 1 << self.n), dtype=complex)
+        idx = np.arange(1 << self.n)
+        for w in range(self.n):
+            if w == skip:
+                continue
+            bit = (idx >> (self.n - 1 - w)) & 1
+            out *= v[:, w, :][:, bit]
+        return out
+
+    def prefix_lambda(self, v, lam, acc):
+        """Couplings of the prefix groups at the prefix boundary:
+        Lambda_w(a) = sum_{j: bit_w(j) = a} conj(lam_j) prod_{w' != w} v_w'(bit_w'(j))."""
+        pre = S.section(self.w, S.SEC_PREFIX, 4)
+        idx = np.arange(1 << self.n)
+        for w, row in enumerate(pre):
+            gid, slot = int(row[0]), int(row[1])
+            if gid < 0 or slot < 0:
+                continue
+            Q = self.product_state(v, skip=w)
+            bit = (idx >> (self.n - 1 - w)) & 1
+            L = np.stack([np.sum(np.conj(lam[:, bit == a]) * Q[:, bit == a], axis=1) for a in (0, 1)], axis=1)
+            acc[gid] = acc.get(gid, 0) + L
+
     # -- whole program -----------------------------------------------------------------------
     def gradient(self, theta, x, batch, weights=None):
         n = self.n
         theta = np.zeros(0) if theta is None else np.asarray(theta, float)
         x = np.zeros((batch, 0)) if x is None else np.asarray(x, float)
         wts = np.ones(n) if weights is None else np.asarray(weights, float)
-        psi = np.zeros((batch, 1 << n), dtype=complex)
-        psi[:, 0] = 1
+        prefix = bool(int(self.w[25]))
+        v = self.prefix_vectors(theta, x, batch) if prefix else None
+        if prefix:
+            psi = self.product_state(v)
+        else:
+            psi = np.zeros((batch, 1 << n), dtype=complex)
+            psi[:, 0] = 1
         lam = np.zeros_like(psi)
         acc, zq = {}, np.zeros((batch, n))
         Pn = len(self.passes)
@@ -305,6 +348,8 @@ class Emulator:
         self.run_pass(Pn - 1, "turn", psi, lam, theta, x, wts, acc, zq)
         for pi in range(Pn - 2, -1, -1):
             self.run_pass(pi, "bwd", psi, lam, theta, x, wts, acc, zq)
+        if prefix:
+            self.prefix_lambda(v, lam, acc)
         grads = np.zeros((batch, self.prog.trainable_count))
         egrads = np.zeros((batch, self.prog.encoding_count))
         for gid, m in acc.items():
@@ -329,6 +374,11 @@ class Emulator:
         grp, mats = group_gate_mats(self.w, self.fv, theta, x, gid)
         d = 1 << int(grp[0])
         diag = bool(int(grp[1]))
+        if int(grp[12]):  # prefix group: M_ab = Lambda(a) v(b), v = U|0>
+            U0 = group_unitary(self.w, self.fv, theta, x, gid)
+            v = U0[..., :, 0]
+            m = m[:, :, None] * (v[:, None, :] if v.ndim == 2 else v[None, None, :])
+            diag = False
         if diag:
             mm = np.zeros(m.shape[:1] + (d, d), dtype=complex)
             for e in range(d):

@@ -205,3 +205,17 @@ def test_build_plan_real_timing_and_replay():
     b = gradient(wl.circuit, wl.theta, wl.x, batch=4, weights=wl.weights)
     np.testing.assert_allclose(a.zq, b.zq, atol=1e-6)
     assert_grads_close(a.grads, b.grads)
+
+
+@pytest.mark.parametrize("cfg,n,b", [(1, 8, 5), (2, 14, 3), (3, 13, 2), (4, 13, 2), (5, 14, 2)])
+def test_product_state_prefix_engine(cfg, n, b):
+    """Synthesized product-state prefix + Lambda couplings vs the plain program vs oracle."""
+    wl = make_workload(cfg, n=n, batch=b)
+    ref = orc.gradient(wl.circuit, wl.theta, wl.x, batch=b, weights=wl.weights)
+    for prefix in (True, False):
+        eng = Engine(wl.circuit, prefix=prefix)
+        assert eng.prefix == prefix
+        r = eng.fwd_bwd(wl.theta, wl.x, batch=b, weights=wl.weights)
+        np.testing.assert_allclose(r["zq"].cpu().numpy(), ref["zq"], atol=Z_TOL)
+        assert_grads_close(r["grads"].cpu().numpy(), ref["grads"])
+        assert_grads_close(r["encoding_grads"].cpu().numpy(), ref["encoding_grads"], "encoding")

@@ -81,3 +81,26 @@ def test_isolated_layers_keep_semantics(cfg):
     res = Emulator(prog).gradient(wl.theta, wl.x, 2, wl.weights)
     ref = orc.gradient(wl.circuit, wl.theta, wl.x, batch=2, weights=wl.weights)
     _cmp(res, ref, atol=1e-8)  # isolated RZ layers become diagonal runs: 2^-32-turn angle grid
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("M,R", [(6, 2), (4, 2)])
+def test_product_state_prefix(cfg, M, R):
+    """The first group of every wire (single-qubit) is synthesized as a product state; its
+    gradient comes from Lambda couplings at the prefix boundary."""
+    wl = make_workload(cfg, n=6, batch=3)
+    prog = S.compile_circuit(wl.circuit, M=M, R=R, prefix=True)
+    executed = {gid for pp in prog.passes for gid in pp.groups}
+    assert prog.prefix and not (set(prog.prefix.values()) & executed)
+    res = Emulator(prog).gradient(wl.theta, wl.x, 3, wl.weights)
+    ref = orc.gradient(wl.circuit, wl.theta, wl.x, batch=3, weights=wl.weights)
+    _cmp(res, ref, atol=1e-8)
+
+
+@pytest.mark.parametrize("c", range(6))
+def test_random_circuits_prefix(c):
+    gold = load_golden("random_circuits")
+    circ = rebuild_random(gold[f"c{c}_spec"])
+    prog = S.compile_circuit(circ, M=4, R=2, prefix=True)
+    res = Emulator(prog).gradient(gold[f"c{c}_theta"], gold[f"c{c}_x"], 3, gold[f"c{c}_w"])
+    _cmp(res, {k[len(f"c{c}_"):]: v for k, v in gold.items() if k.startswith(f"c{c}_")}, atol=1e-8)
