@@ -616,10 +616,69 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
             if k < last:
                 _emit_exchange(w, P, k, k + 1, nv)
 
+    obs = getattr(prog, "obs", None) if mode == MODE_TURN else None
+
+    def obs_parts(k, q):
+        """(register-bit mask over register index, thread local-bit mask, tile physical mask, c)
+        of the folded observable parity of wire q in layout k."""
+        m, c = obs[q]
+        ph = P.pp.phases[k]
+        rmask = sum(1 << kk for kk in range(P.R) if (m >> P.pbit[ph.regs[kk]]) & 1)
+        tmask = sum(1 << lb for lb in ph.threads if (m >> P.pbit[lb]) & 1)
+        nmask = sum(1 << p for p in P.nbit if (m >> p) & 1)
+        return rmask, tmask, nmask, c
+
+    def emit_obs_signs(k):
+        """per-thread sign of every wire's parity: thread bits, tile bits and the constant"""
+        for q in range(P.n):
+            rmask, tmask, nmask, c = obs_parts(k, q)
+            terms = [f"(__popc(tp{k} & {tmask}u) & 1)" if tmask else "0",
+                     f"(__popcll(tbase & {nmask}ull) & 1)" if nmask else "0", str(c)]
+            w(f"const float sg{q} = ((({' ^ '.join(terms)}) & 1) ? -1.f : 1.f);")
+
+    def emit_zpart_obs(k):
+        w("{")
+        w.ind += 1
+        emit_obs_signs(k)
+        w(f"float pz[{P.n + 1}];")
+        w("float S_ = 0.f;")
+        for i in range(P.NR):
+            w(f"const float pr{i} = v[0][{i}].x * v[0][{i}].x + v[0][{i}].y * v[0][{i}].y;")
+        w(f"S_ = {' + '.join(f'pr{i}' for i in range(P.NR))};")
+        for q in range(P.n):
+            rmask = obs_parts(k, q)[0]
+            terms = " ".join(f"{'-' if bin(i & rmask).count('1') & 1 else '+'} pr{i}" for i in range(P.NR))
+            w(f"pz[{q}] = sg{q} * (0.f {terms});")
+        w(f"pz[{P.n}] = S_;")
+        w(f"warp_sum<NT, {P.n + 1}>(pz);")
+        w.block("if ((tid & 31) == 0)")
+        w("float* zw = s_zw + warp * 32;")
+        for q in range(P.n):
+            w(f"zw[{P.n - 1 - q}] += pz[{q}];")
+        w(f"zw[{P.n}] += pz[{P.n}];")
+        w.end()
+        w.ind -= 1
+        w("}")
+
+    def emit_lambda_obs(k):
+        w("{")
+        w.ind += 1
+        emit_obs_signs(k)
+        for q in range(P.n):
+            w(f"const float ws{q} = sg{q} * (A.wts ? (float)A.wts[{q}] : 1.f);")
+        for i in range(P.NR):
+            terms = " ".join(f"{'-' if bin(i & obs_parts(k, q)[0]).count('1') & 1 else '+'} ws{q}" for q in range(P.n))
+            w(f"{{ const float o = 0.f {terms}; v[1][{i}] = make_float2(o * v[0][{i}].x, o * v[0][{i}].y); }}")
+        w.ind -= 1
+        w("}")
+
     def emit_zpart(k):
         # <Z> partials without block barriers: warp shuffle tree, then lane 0 of each warp adds
         # into its own per-warp slot (indexed by physical bit; [n] = norm). Reduced over warps in
         # fp64 once per CTA, after the tile loop.
+        if obs:
+            emit_zpart_obs(k)
+            return
         ph = P.pp.phases[k]
         w("{")
         w.ind += 1
@@ -649,6 +708,9 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
         w("}")
 
     def emit_lambda_init(k):
+        if obs:
+            emit_lambda_obs(k)
+            return
         ph = P.pp.phases[k]
         w("{")
         w.ind += 1

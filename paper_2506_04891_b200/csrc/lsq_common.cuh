@@ -15,7 +15,7 @@ constexpr int MAGIC = 0x4C535131;
 constexpr int HDR_WORDS = 32, GATE_WORDS = 8, GROUP_WORDS = 16, PASS_WORDS = 24,
               PHASE_WORDS = 24, OP_WORDS = 8, SUB_WORDS = 8, PGROUP_WORDS = 4;
 constexpr int SEC_GATES = 0, SEC_GROUPS = 1, SEC_PASSES = 2, SEC_PHASES = 3, SEC_OPS = 4,
-              SEC_SUBS = 5, SEC_PGROUPS = 6, SEC_PREFIX = 7, N_SECTIONS = 8;
+              SEC_SUBS = 5, SEC_PGROUPS = 6, SEC_PREFIX = 7, SEC_OBS = 8, N_SECTIONS = 9;
 constexpr int OP_U1 = 1, OP_U2 = 2, OP_DRUN = 3, OP_PX = 4, OP_PCX = 5;
 constexpr int SRC_NONE = 0, SRC_REG = 1, SRC_THREAD = 2, SRC_NONLOCAL = 3;
 constexpr int ENC_FLAG = 1 << 30;
@@ -28,7 +28,7 @@ enum { PW_M = 0, PW_R, PW_NPH, PW_PH0, PW_MASK, PW_NGRP, PW_PG0, PW_MATF, PW_SLO
 // group word fields
 enum { GW_ARITY = 0, GW_DIAG, GW_PERROW, GW_NG, GW_G0, GW_WA, GW_WB, GW_SLOT, GW_SLOTF,
        GW_MATF, GW_GRAD, GW_ROWIDX, GW_PREFIX };
-constexpr int HDR_NPERROW = 24, HDR_PREFIX = 25;
+constexpr int HDR_NPERROW = 28, HDR_PREFIX = 29, HDR_OBS = 30;
 // phase words: [0,5) register local bits, [5,21) thread local bits, 21 op0, 22 nops
 constexpr int PH_OP0 = 21, PH_NOPS = 22;
 

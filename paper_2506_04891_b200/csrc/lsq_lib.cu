@@ -256,7 +256,7 @@ struct JitKernel {
 struct lsq_program {
   std::vector<JitKernel> jit;  // [pass * 3 + mode], fn == nullptr -> generic kernel
   std::vector<cudaLibrary_t> jit_libs;
-  int n, T, E, npasses, ngroups, slot_total, nperrow, prefix = 0;
+  int n, T, E, npasses, ngroups, slot_total, nperrow, prefix = 0, obs = 0;
   int* d_words = nullptr;
   double* d_fvals = nullptr;
   std::vector<int> words;
@@ -368,8 +368,8 @@ int launch_pass(lsq_program* P, int pi_idx, int mode, int flags, int batch, cons
   const int NV = mode == MODE_FWD ? 1 : 2;
   const KEntry& k = NV == 1 ? pi.k1 : pi.k2;
   const bool have_jit = !P->jit.empty() && P->jit[pi_idx * 3 + mode].fn;
-  if (P->prefix && !have_jit)
-    return fail(LSQ_EPLAN, "programs with a synthesized product-state prefix need the specialised kernels");
+  if ((P->prefix || P->obs) && !have_jit)
+    return fail(LSQ_EPLAN, "programs with a synthesized prefix or a folded observable need the specialised kernels");
   if (!k.fn && !have_jit)
     return fail(LSQ_EPLAN, "no kernel for pass " + std::to_string(pi_idx) + " (M=" + std::to_string(pi.M) +
                                ", R=" + std::to_string(pi.R) + "): attach the specialised kernels");
@@ -493,6 +493,7 @@ int lsq_program_create(const int32_t* words, int64_t n_words, const double* fval
   P->ngroups = W[7];
   P->nperrow = W[HDR_NPERROW];
   P->prefix = W[HDR_PREFIX];
+  P->obs = W[HDR_OBS];
   if (P->n < 1 || P->n > 30) {
     delete P;
     return fail(LSQ_EINVAL, "n out of range (1..30)");

@@ -127,7 +127,7 @@ class Engine:
     """A circuit compiled for the device; the object behind the drop-in API."""
 
     def __init__(self, circuit, M: int | None = None, R: int | None = None, device=None, jit=None,
-                 isolate=(), prefix=None):
+                 isolate=(), prefix=None, fold=None):
         self.device = torch.device(device if device is not None else "cuda")
         if self.device.type != "cuda":
             raise ValueError("the engine runs on CUDA devices only")
@@ -146,8 +146,14 @@ class Engine:
             prefix = jit and os.environ.get("LSQ_PREFIX", "1") != "0"
         if prefix and not jit:
             raise ValueError("the product-state prefix needs the specialised (JIT) kernels")
-        self.program = compile_circuit(circuit, M=M, R=R, isolate=isolate, prefix=prefix)
-        self.prefix = bool(self.program.prefix)
+        # trailing diagonal / permutation groups folded into the observable: gradient-type
+        # programs only (same JIT requirement as the prefix)
+        if fold is None:
+            fold = bool(prefix) and os.environ.get("LSQ_FOLD", "1") != "0"
+        if fold and not jit:
+            raise ValueError("the folded observable needs the specialised (JIT) kernels")
+        self.program = compile_circuit(circuit, M=M, R=R, isolate=isolate, prefix=prefix, fold=fold)
+        self.prefix = bool(self.program.prefix) or bool(self.program.obs)
         self.native = NativeProgram(self.program, self.device)
         if jit:
             self.native.attach_jit()
@@ -202,6 +208,9 @@ class Engine:
     def forward(self, trainable=None, encoding=None, state=None, batch=None, weights=None, want_z=False):
         """Evolve `state` ((B, 2^n) complex64 CUDA tensor, or None = |0..0> with `batch` rows)
         through the circuit into a NEW tensor. Returns (psi, zq, value)."""
+        if self.program.obs:
+            raise ValueError("this program folds its trailing permutations/diagonals into the "
+                             "observable (gradient programs); compile with fold=False to get states")
         if state is not None:
             if self.prefix:
                 raise ValueError("this program synthesizes its |0..0> prefix; compile with prefix=False "

@@ -128,7 +128,8 @@ def time_program(circuit, batch: int, objective: "Objective" = None, M=None, iso
         raise ValueError("reps must be at least 1")
     if warmup < 0:
         raise ValueError("warmup cannot be negative")
-    eng = Engine(circuit, M=M, isolate=isolate, device=device)
+    eng = Engine(circuit, M=M, isolate=isolate, device=device,
+                 fold=False if objective is Objective.FORWARD else None)
     th, x = _draw(circuit, batch, seed)
     th_d = None if th is None else torch.as_tensor(th, device=eng.device)
     x_d = None if x is None else torch.as_tensor(x, device=eng.device)

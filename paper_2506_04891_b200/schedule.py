@@ -138,6 +138,7 @@ class Group:
     wires: tuple  # group basis order (first wire = more significant local bit)
     gates: list = field(default_factory=list)  # list of (GateRef, reversed: bool)
     prefix: bool = False  # synthesized product-state prefix (not executed by any pass)
+    trailing: bool = False  # folded into the observable (not executed, zero gradient)
 
     @property
     def arity(self) -> int:
@@ -177,7 +178,7 @@ class Group:
 
     @property
     def slot_floats(self) -> int:
-        if not self.needs_grad:
+        if not self.needs_grad or self.trailing:
             return 0
         if self.prefix:
             return 4  # Lambda(0), Lambda(1): M_ab = Lambda(a) v(b), v = U|0>
@@ -505,8 +506,52 @@ def prefix_groups(groups) -> dict:
     return {w: g.gid for w, g in first.items() if g.arity == 1}
 
 
+def trailing_groups(groups) -> tuple[list, list]:
+    """Groups after which only diagonal or parameter-free permutation groups touch their wires.
+    Returns (trailing gids, the trailing permutation groups in application order).
+
+    Trailing diagonal groups commute with the observable sum_q w_q Z_q: they change neither
+    <Z_q> nor any gradient (theirs are structurally zero). Trailing permutations relabel the
+    basis: Z_q measured after them is the parity (-1)^(a_q . j + c_q) of the state before them.
+    """
+    nt_wires: set = set()
+    trailing = []
+    for g in reversed(groups):
+        foldable = g.diag or g.perm_ops is not None
+        if foldable and not (set(g.wires) & nt_wires):
+            trailing.append(g.gid)
+        else:
+            nt_wires |= set(g.wires)
+    tset = set(trailing)
+    perms = [g for g in groups if g.gid in tset and not g.diag]
+    return sorted(tset), perms
+
+
+def observable_masks(perms, n: int):
+    """Affine GF(2) map of the trailing permutations: for every wire q, (mask_q, c_q) over
+    PHYSICAL index bits such that bit_q(pi(j)) = parity(mask_q & j) ^ c_q."""
+    rows = [1 << w for w in range(n)]  # rows[w]: set of source wires (bit w') feeding wire w
+    const = [0] * n
+    for g in perms:
+        for prim in g.perm_ops:
+            if prim[0] == "x":
+                const[g.wires[prim[1]]] ^= 1
+            else:
+                c, t = g.wires[prim[1]], g.wires[prim[2]]
+                rows[t] ^= rows[c]
+                const[t] ^= const[c]
+    masks = []
+    for q in range(n):
+        m = 0
+        for w in range(n):
+            if (rows[q] >> w) & 1:
+                m |= 1 << (n - 1 - w)
+        masks.append((m, const[q]))
+    return masks
+
+
 def compile_circuit(circuit, M: int | None = None, R: int | None = None, isolate=(),
-                    prefix: bool = False) -> Program:
+                    prefix: bool = False, fold: bool = False) -> Program:
     """Compile a (reference-compatible) circuit into a pass program.
 
     `isolate`: layer indices executed with pass boundaries of their own (planner variant
@@ -531,13 +576,21 @@ def compile_circuit(circuit, M: int | None = None, R: int | None = None, isolate
         segs.append(cur)
     groups, passes = [], []
     pre: dict = {}
+    obs = None
     for si, seg in enumerate(segs):
         grp = fuse_groups(seg)
         preds = group_preds(grp)
-        skip = ()
+        skip = set()
         if prefix and si == 0:
             pre = prefix_groups(grp)
-            skip = set(pre.values())
+            skip |= set(pre.values())
+        if fold and si == len(segs) - 1:
+            tr, perms = trailing_groups(grp)
+            tr = [g for g in tr if g not in skip]
+            skip |= set(tr)
+            obs = observable_masks(perms, n)
+            for gid in tr:
+                grp[gid].trailing = True
         seg_passes = schedule_passes(grp, n, M, skip=skip) if (grp or not passes) else []
         need2 = any(g.arity == 2 and not g.diag for g in grp)
         for pp in seg_passes:
@@ -576,6 +629,7 @@ def compile_circuit(circuit, M: int | None = None, R: int | None = None, isolate
     prog = Program(n, groups, passes, T, E, slot_base, total, M=M, gates=gates)
     prog.isolate = tuple(sorted(iso))
     prog.prefix = {w: gid for w, gid in pre.items()}
+    prog.obs = obs
     encode(prog)
     return prog
 
@@ -711,9 +765,11 @@ def encode(prog: Program) -> None:
     pre = getattr(prog, "prefix", {}) or {}
     pslots = prog.enc[0]["prefix_slots"] if prog.enc else {}
     prefix_w = [[pre.get(w, -1), pslots.get(pre.get(w, -1), -1), 0, 0] for w in range(n)] if pre else []
+    obs = getattr(prog, "obs", None)
+    obs_w = [[m, c, 0, 0] for (m, c) in obs] if obs else []
     hdr = [0] * HDR_WORDS
-    sections = [gates_w, group_w, pass_w, phase_w, op_w, sub_w, pgrp_w, prefix_w]
-    widths = [GATE_WORDS, GROUP_WORDS, PASS_WORDS, PHASE_WORDS, OP_WORDS, SUB_WORDS, 4, 4]
+    sections = [gates_w, group_w, pass_w, phase_w, op_w, sub_w, pgrp_w, prefix_w, obs_w]
+    widths = [GATE_WORDS, GROUP_WORDS, PASS_WORDS, PHASE_WORDS, OP_WORDS, SUB_WORDS, 4, 4, 4]
     hdr[0] = MAGIC
     hdr[1] = 1
     hdr[2] = n
@@ -722,8 +778,9 @@ def encode(prog: Program) -> None:
     hdr[5] = prog.slot_total
     hdr[6] = len(prog.passes)
     hdr[7] = len(prog.groups)
-    hdr[24] = rowidx  # number of per-row (encoding) groups
-    hdr[25] = int(bool(pre))  # product-state prefix synthesized by the first pass
+    hdr[28] = rowidx  # number of per-row (encoding) groups
+    hdr[29] = int(bool(pre))  # product-state prefix synthesized by the first pass
+    hdr[30] = int(bool(obs))  # observable folded through trailing permutations (section 8)
     off = HDR_WORDS
     flat = []
     for si, (sec, wd) in enumerate(zip(sections, widths)):
@@ -744,8 +801,8 @@ def section(words: np.ndarray, idx: int, width: int) -> np.ndarray:
     return words[off : off + cnt * width].reshape(cnt, width)
 
 
-SEC_GATES, SEC_GROUPS, SEC_PASSES, SEC_PHASES, SEC_OPS, SEC_SUBS, SEC_PGROUPS, SEC_PREFIX = range(8)
-SEC_WIDTH = [GATE_WORDS, GROUP_WORDS, PASS_WORDS, PHASE_WORDS, OP_WORDS, SUB_WORDS, 4, 4]
+SEC_GATES, SEC_GROUPS, SEC_PASSES, SEC_PHASES, SEC_OPS, SEC_SUBS, SEC_PGROUPS, SEC_PREFIX, SEC_OBS = range(9)
+SEC_WIDTH = [GATE_WORDS, GROUP_WORDS, PASS_WORDS, PHASE_WORDS, OP_WORDS, SUB_WORDS, 4, 4, 4]
 
 
 def describe(prog: Program) -> str:

@@ -274,11 +274,22 @@ class Emulator:
                 fwd_phase(ph)
         if mode == "turn":
             prob = np.abs(P) ** 2
-            # <Z_q> partials and lam = O psi
+            # <Z_q> partials and lam = O psi; with a folded observable Z_q reads the parity of
+            # (mask_q & j) ^ c_q (trailing permutations)
             full = idx  # (T, D) physical index
             O = np.zeros(full.shape)
+            obs = S.section(self.w, S.SEC_OBS, 4) if int(self.w[30]) else None
             for q in range(self.n):
-                s = 1.0 - 2.0 * _bit(full, self.n - 1 - q)
+                if obs is None:
+                    b = _bit(full, self.n - 1 - q)
+                else:
+                    m, c = int(obs[q][0]), int(obs[q][1])
+                    b = np.zeros_like(full)
+                    for pbit in range(self.n):
+                        if (m >> pbit) & 1:
+                            b ^= _bit(full, pbit)
+                    b ^= c
+                s = 1.0 - 2.0 * b
                 zq[:, q] += np.sum(prob * s[None], axis=(1, 2))
                 O += wts[q] * s
             Lm = P * O[None]
@@ -294,7 +305,7 @@ class Emulator:
         """v[b, w] = U_w |0> for wires with a prefix group, |0> otherwise (B, n, 2)."""
         v = np.zeros((batch, self.n, 2), dtype=complex)
         v[:, :, 0] = 1
-        pre = S.section(self.w, S.SEC_PREFIX, 4) if int(self.w[25]) else []
+        pre = S.section(self.w, S.SEC_PREFIX, 4) if int(self.w[29]) else []
         for w, row in enumerate(pre):
             gid = int(row[0])
             if gid >= 0:
@@ -333,7 +344,7 @@ class Emulator:
         theta = np.zeros(0) if theta is None else np.asarray(theta, float)
         x = np.zeros((batch, 0)) if x is None else np.asarray(x, float)
         wts = np.ones(n) if weights is None else np.asarray(weights, float)
-        prefix = bool(int(self.w[25]))
+        prefix = bool(int(self.w[29]))
         v = self.prefix_vectors(theta, x, batch) if prefix else None
         if prefix:
             psi = self.product_state(v)

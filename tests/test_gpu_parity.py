@@ -122,7 +122,7 @@ def test_x_swap_bit_exact():
 @pytest.mark.parametrize("M", [None, 4, 5])
 def test_forward_state_matches_oracle(M):
     wl = make_workload(5, n=7, batch=2)
-    eng = Engine(wl.circuit, M=M)
+    eng = Engine(wl.circuit, M=M, fold=False)
     out, zq, val = eng.forward(wl.theta, wl.x, batch=2, weights=wl.weights, want_z=True)
     ref = orc.apply_circuit(wl.circuit, wl.theta, wl.x, batch=2)
     np.testing.assert_allclose(out.cpu().numpy(), ref, atol=2e-6)
@@ -212,9 +212,9 @@ def test_product_state_prefix_engine(cfg, n, b):
     """Synthesized product-state prefix + Lambda couplings vs the plain program vs oracle."""
     wl = make_workload(cfg, n=n, batch=b)
     ref = orc.gradient(wl.circuit, wl.theta, wl.x, batch=b, weights=wl.weights)
-    for prefix in (True, False):
-        eng = Engine(wl.circuit, prefix=prefix)
-        assert eng.prefix == prefix
+    for prefix, fold in ((True, True), (True, False), (False, False)):
+        eng = Engine(wl.circuit, prefix=prefix, fold=fold)
+        assert bool(eng.program.prefix) == prefix and bool(eng.program.obs) == fold
         r = eng.fwd_bwd(wl.theta, wl.x, batch=b, weights=wl.weights)
         np.testing.assert_allclose(r["zq"].cpu().numpy(), ref["zq"], atol=Z_TOL)
         assert_grads_close(r["grads"].cpu().numpy(), ref["grads"])

@@ -104,3 +104,27 @@ def test_random_circuits_prefix(c):
     prog = S.compile_circuit(circ, M=4, R=2, prefix=True)
     res = Emulator(prog).gradient(gold[f"c{c}_theta"], gold[f"c{c}_x"], 3, gold[f"c{c}_w"])
     _cmp(res, {k[len(f"c{c}_"):]: v for k, v in gold.items() if k.startswith(f"c{c}_")}, atol=1e-8)
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+def test_observable_folding(cfg):
+    """Trailing diagonal / permutation groups are folded into the observable."""
+    wl = make_workload(cfg, n=6, batch=3)
+    prog = S.compile_circuit(wl.circuit, M=4, R=2, prefix=True, fold=True)
+    folded = [g.gid for g in prog.groups if g.trailing]
+    executed = {gid for pp in prog.passes for gid in pp.groups}
+    assert not (set(folded) & executed)
+    if cfg in (1, 2, 5):  # circuits ending with a CNOT ring (+ ZZ)
+        assert folded
+    res = Emulator(prog).gradient(wl.theta, wl.x, 3, wl.weights)
+    ref = orc.gradient(wl.circuit, wl.theta, wl.x, batch=3, weights=wl.weights)
+    _cmp(res, ref, atol=1e-8)
+
+
+@pytest.mark.parametrize("c", range(6))
+def test_random_circuits_folding(c):
+    gold = load_golden("random_circuits")
+    circ = rebuild_random(gold[f"c{c}_spec"])
+    prog = S.compile_circuit(circ, M=4, R=2, prefix=True, fold=True)
+    res = Emulator(prog).gradient(gold[f"c{c}_theta"], gold[f"c{c}_x"], 3, gold[f"c{c}_w"])
+    _cmp(res, {k[len(f"c{c}_"):]: v for k, v in gold.items() if k.startswith(f"c{c}_")}, atol=1e-8)
