@@ -38,6 +38,7 @@ _SIGS = {
     "lsq_set_profiling": (_I, [_P, _I]),
     "lsq_last_pass_times": (_I, [_P, _P, _I, _P]),
     "lsq_last_launch_count": (_I, [_P]),
+    "lsq_jit_compiler": (_I, [_c.c_char_p, _I]),
 }
 
 EXPORTS = tuple(_SIGS)
@@ -89,3 +90,9 @@ def require_cuda():
     if not torch.cuda.is_available():
         raise NativeUnavailable("no CUDA device visible: the engine has no CPU fallback")
     load_library()
+
+
+def jit_compiler() -> str:
+    buf = ctypes.create_string_buffer(1024)
+    lib().lsq_jit_compiler(buf, 1024)
+    return buf.value.decode()

@@ -2,7 +2,10 @@
 // forward / forward+adjoint drivers, and the small auxiliary kernels (group tables,
 // deterministic fp64 reductions, coupling contraction).
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <limits.h>
 #include <nvrtc.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <cstdio>
@@ -568,37 +571,94 @@ bool read_file(const std::string& path, std::string& out) {
   return !out.empty();
 }
 
+// NVRTC is resolved at run time from the CUDA toolkit this library was built against (absolute
+// path, RTLD_LOCAL): a process that imported torch first already has torch's bundled
+// libnvrtc.so.12 (an older 12.x) loaded under the same SONAME, and that ptxas does not fold the
+// FFMA2 lane swap/negation into operand modifiers (measured: 1148 MOVs vs 6 in one kernel).
+struct Nvrtc {
+  decltype(&nvrtcCreateProgram) create = nullptr;
+  decltype(&nvrtcCompileProgram) compile = nullptr;
+  decltype(&nvrtcGetProgramLogSize) log_size = nullptr;
+  decltype(&nvrtcGetProgramLog) log = nullptr;
+  decltype(&nvrtcGetCUBINSize) cubin_size = nullptr;
+  decltype(&nvrtcGetCUBIN) cubin = nullptr;
+  decltype(&nvrtcDestroyProgram) destroy = nullptr;
+  decltype(&nvrtcVersion) version = nullptr;
+  std::string path, err;
+  bool ok = false;
+};
+
+#ifndef LSQ_NVRTC_DEFAULT
+#define LSQ_NVRTC_DEFAULT "/usr/local/cuda/lib64/libnvrtc.so.12"
+#endif
+
+const Nvrtc& nvrtc() {
+  static Nvrtc N;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* env = getenv("LSQ_NVRTC");
+    std::string want = env && *env ? env : LSQ_NVRTC_DEFAULT;
+    char real[PATH_MAX];
+    if (realpath(want.c_str(), real)) want = real;
+    void* h = dlopen(want.c_str(), RTLD_NOW | RTLD_LOCAL);
+    if (!h) {
+      N.err = std::string("dlopen(") + want + "): " + dlerror();
+      return;
+    }
+    N.path = want;
+    N.create = (decltype(N.create))dlsym(h, "nvrtcCreateProgram");
+    N.compile = (decltype(N.compile))dlsym(h, "nvrtcCompileProgram");
+    N.log_size = (decltype(N.log_size))dlsym(h, "nvrtcGetProgramLogSize");
+    N.log = (decltype(N.log))dlsym(h, "nvrtcGetProgramLog");
+    N.cubin_size = (decltype(N.cubin_size))dlsym(h, "nvrtcGetCUBINSize");
+    N.cubin = (decltype(N.cubin))dlsym(h, "nvrtcGetCUBIN");
+    N.destroy = (decltype(N.destroy))dlsym(h, "nvrtcDestroyProgram");
+    N.version = (decltype(N.version))dlsym(h, "nvrtcVersion");
+    N.ok = N.create && N.compile && N.log_size && N.log && N.cubin_size && N.cubin && N.destroy;
+    if (!N.ok) N.err = "missing NVRTC symbols in " + want;
+  });
+  return N;
+}
+
 // NVRTC: source -> sm_100a cubin (with an optional on-disk cache keyed by the source hash)
 int jit_compile(const std::string& src, const std::string& cache_dir, std::string& cubin, std::string& log) {
+  const Nvrtc& R = nvrtc();
+  if (!R.ok) {
+    log = R.err;
+    return 1;
+  }
   std::string key;
   if (!cache_dir.empty()) {
     char buf[40];
-    snprintf(buf, sizeof buf, "%016llx", (unsigned long long)fnv1a(src.data(), src.size()));
+    int maj = 0, min = 0;
+    if (R.version) R.version(&maj, &min);
+    const std::string keyed = src + "\n// nvrtc " + std::to_string(maj) + "." + std::to_string(min);
+    snprintf(buf, sizeof buf, "%016llx", (unsigned long long)fnv1a(keyed.data(), keyed.size()));
     key = cache_dir + "/lsq_" + buf + ".cubin";
     if (read_file(key, cubin)) return 0;
   }
   nvrtcProgram prog;
-  if (nvrtcCreateProgram(&prog, src.c_str(), "lsq_jit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) {
+  if (R.create(&prog, src.c_str(), "lsq_jit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) {
     log = "nvrtcCreateProgram failed";
     return 1;
   }
   const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo", "-DNDEBUG"};
-  nvrtcResult rc = nvrtcCompileProgram(prog, 4, opts);
+  nvrtcResult rc = R.compile(prog, 4, opts);
   size_t ls = 0;
-  nvrtcGetProgramLogSize(prog, &ls);
+  R.log_size(prog, &ls);
   if (ls > 1) {
     log.resize(ls);
-    nvrtcGetProgramLog(prog, &log[0]);
+    R.log(prog, &log[0]);
   }
   if (rc != NVRTC_SUCCESS) {
-    nvrtcDestroyProgram(&prog);
+    R.destroy(&prog);
     return 1;
   }
   size_t cs = 0;
-  nvrtcGetCUBINSize(prog, &cs);
+  R.cubin_size(prog, &cs);
   cubin.resize(cs);
-  nvrtcGetCUBIN(prog, &cubin[0]);
-  nvrtcDestroyProgram(&prog);
+  R.cubin(prog, &cubin[0]);
+  R.destroy(&prog);
   if (!key.empty()) {
     std::string tmp = key + ".tmp" + std::to_string((unsigned long long)std::hash<std::thread::id>{}(std::this_thread::get_id()));
     std::ofstream f(tmp, std::ios::binary);
@@ -696,6 +756,14 @@ int lsq_last_pass_times(const lsq_program* P, float* ms, int cap, int* kinds) {
 }
 
 int lsq_last_launch_count(const lsq_program* P) { return P ? P->launches : -1; }
+
+int lsq_jit_compiler(char* buf, int buflen) {
+  const Nvrtc& R = nvrtc();
+  int maj = 0, min = 0;
+  if (R.ok && R.version) R.version(&maj, &min);
+  snprintf(buf, buflen, "%s|%d.%d|%s", R.ok ? R.path.c_str() : "unavailable", maj, min, R.err.c_str());
+  return R.ok ? LSQ_OK : LSQ_ECUDA;
+}
 
 int lsq_forward(const lsq_program* Pc, int batch, const double* theta, const double* x, int x_stride,
                 const double* w, const void* psi_in, void* psi_out, double* zq, double* value,

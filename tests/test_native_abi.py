@@ -51,3 +51,20 @@ def test_status_codes_map_to_reference_exceptions():
         _native.check(3)
     with pytest.raises(RuntimeError):
         _native.check(4)
+
+
+def test_jit_uses_toolkit_nvrtc_not_first_loaded():
+    """The JIT must use the toolkit's NVRTC even when torch's bundled (older) libnvrtc.so.12
+    is already loaded in the process: the older ptxas leaves the FFMA2 lane swaps as MOVs."""
+    import glob
+    import os
+
+    import torch
+
+    for p in glob.glob(os.path.join(os.path.dirname(torch.__file__), "..", "nvidia", "cuda_nvrtc", "lib",
+                                    "libnvrtc.so*")):
+        ctypes.CDLL(p, mode=ctypes.RTLD_GLOBAL)
+    path, ver, err = _native.jit_compiler().split("|", 2)
+    assert not err, err
+    maj, mnr = map(int, ver.split("."))
+    assert (maj, mnr) >= (12, 9), (path, ver)
