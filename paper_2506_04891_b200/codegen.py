@@ -191,42 +191,107 @@ def _src_expr(sw, P, tp_var):
     return "none", None
 
 
+PAT_U1 = (1, 3, 4, 7)    # u1_coupling_h: {Im c00, s, t, Im c11} -> M'00.y, M'01.y, M'10.x, M'11.y
+PAT_DIAG = (1, 3, 5, 7)  # diagonal runs: Im c_e -> M'_e.y (the real parts never reach Re(W M))
+
+
+class _Coup:
+    """Backward couplings as 4-float half-blocks (anti-Hermitian projections, see
+    u1_coupling_h); two half-blocks share one 8-value warp reduce-scatter. A half-block is
+    (array name, slot base, pattern, number of real values); values past `nreal` are zeros
+    that land on the pattern's addresses, so a pairing is refused when such a zero write would
+    hit an address the other half writes in the same instruction."""
+
+    def __init__(self, P):
+        self.P = P
+        self.n = 0
+        self.pending = None
+
+    def new(self, w):
+        name = f"cp{self.n}_"
+        self.n += 1
+        w(f"float {name}[4];")
+        return name
+
+    @staticmethod
+    def _addrs(h):
+        _, base, pat, nreal = h
+        a = [base + o for o in pat]
+        return a[:nreal], a[nreal:]
+
+    def _conflict(self, a, b):
+        ra, za = self._addrs(a)
+        rb, zb = self._addrs(b)
+        return bool(set(za) & set(rb)) or bool(set(zb) & set(ra))
+
+    def push(self, w, name, base, pat, nreal=4):
+        h = (name, base, pat, nreal)
+        a = self.pending
+        self.pending = None
+        if a is not None:
+            if a[3] == 2 and nreal == 2 and a[2] == PAT_DIAG and pat == PAT_DIAG and base == a[1] + 4:
+                nm = self.new(w)
+                w(f"{nm}[0] = {a[0]}[0]; {nm}[1] = {a[0]}[1]; {nm}[2] = {name}[0]; {nm}[3] = {name}[1];")
+                self.pending = (nm, a[1], PAT_DIAG, 4)
+                return
+            if not self._conflict(a, h):
+                self._emit(w, a, h)
+                return
+            self._emit(w, a, None)
+        self.pending = h
+
+    def flush(self, w):
+        if self.pending is not None:
+            a = self.pending
+            self.pending = None
+            self._emit(w, a, None)
+
+    def _emit(self, w, a, b):
+        P = self.P
+        vals = [f"{a[0]}[{k}]" for k in range(4)] + ([f"{b[0]}[{k}]" for k in range(4)] if b else ["0.f"] * 4)
+        init = f"float a8_[8] = {{{', '.join(vals)}}};"
+        if P.NT >= 32:
+            bb = b if b is not None else (None, P.slotf, PAT_DIAG, 0)  # zero half -> padding
+            pv = {PAT_U1: "pu1_", PAT_DIAG: "pdg_"}
+            w(f"{{ {init} warp_accumulate8p<NT>(a8_, wacc + (hi16_ ? {bb[1]} + {pv[bb[2]]} : {a[1]} + {pv[a[2]]})); }}")
+        else:
+            adds = [f"wacc[{a[1] + a[2][k]}] += a8_[{k}];" for k in range(a[3])]
+            if b is not None:
+                adds += [f"wacc[{b[1] + b[2][k]}] += a8_[{4 + k}];" for k in range(b[3])]
+            w(f"{{ {init} warp_sum<NT, 8>(a8_); if ((tid & 31) == 0) {{ {' '.join(adds)} }} }}")
+
+
 def _emit_drun(w, P, op, ph_idx, mode_bwd, nv):
     subs = P.enc["subs"][op[6] : op[6] + op[7]]
     tp = f"tp{ph_idx}"
     R = P.R
     # couplings (backward, before un-applying: conj(l) p is phase invariant)
     if mode_bwd and any(int(s[4]) >= 0 for s in subs):
+        names = {si: P.coup.new(w) for si, s in enumerate(subs) if int(s[4]) >= 0}
         w("{")
         w.ind += 1
         for i in range(P.NR):
-            w(f"const float2 c{i} = cjmul(v[1][{i}], v[0][{i}]);")
-        for s in subs:
+            w(f"const float c{i} = v[1][{i}].x * v[0][{i}].y - v[1][{i}].y * v[0][{i}].x;  // Im conj(l) p")
+        for si, s in enumerate(subs):
             slot = int(s[4])
             if slot < 0:
                 continue
+            nm = names[si]
             ka, ea = _src_expr(s[0], P, tp)
             kb, eb = _src_expr(s[1], P, tp)
             ar = int(s[5])
-            # index of register i: (A bit, B bit) -> e
             terms = {}
             for i in range(P.NR):
                 if ar == 1:
-                    if ka == "reg":
-                        e = (i >> ea) & 1
-                    else:
-                        e = None
+                    e = ((i >> ea) & 1) if ka == "reg" else None
                 else:
                     a = ((i >> ea) & 1) if ka == "reg" else None
                     b = ((i >> eb) & 1) if kb == "reg" else None
                     e = (a, b)
                 terms.setdefault(e, []).append(i)
-            w("{")
-            w.ind += 1
-            w("float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};")
+            w(" ".join(f"{nm}[{k}] = {'-0.f' if k < (1 << ar) else '0.f'};" for k in range(4)))
             for e, idxs in terms.items():
-                sx = " + ".join(f"c{i}.x" for i in idxs)
-                sy = " + ".join(f"c{i}.y" for i in idxs)
+                sy = " + ".join(f"c{i}" for i in idxs)
                 if ar == 1:
                     ix = str(e) if e is not None else ea
                 else:
@@ -237,17 +302,17 @@ def _emit_drun(w, P, op, ph_idx, mode_bwd, nv):
                         b_e = str(e[1]) if e[1] is not None else eb
                         ix = f"(2 * ({a_e}) + ({b_e}))"
                 if ix.isdigit():
-                    w(f"acc[{2 * int(ix)}] += {sx}; acc[{2 * int(ix) + 1}] += {sy};")
+                    w(f"{nm}[{int(ix)}] += {sy};")
                 else:
-                    w(f"{{ const int e_ = {ix}; const float sx_ = {sx}, sy_ = {sy};")
+                    w(f"{{ const int e_ = {ix}; const float sy_ = {sy};")
                     for ee in range(1 << ar):
-                        w(f"  acc[{2 * ee}] += e_ == {ee} ? sx_ : 0.f; acc[{2 * ee + 1}] += e_ == {ee} ? sy_ : 0.f;")
+                        w(f"  {nm}[{ee}] += e_ == {ee} ? sy_ : 0.f;")
                     w("}")
-            w(f"warp_accumulate8<{P.NT}>(acc, wacc + {slot});")
-            w.ind -= 1
-            w("}")
         w.ind -= 1
         w("}")
+        for si, s in enumerate(subs):
+            if int(s[4]) >= 0:
+                P.coup.push(w, names[si], int(s[4]), PAT_DIAG, 1 << int(s[5]))
     # phases
     w("{")
     w.ind += 1
@@ -309,8 +374,9 @@ def _emit_ops(w, P, ph_idx, mode_bwd, nv):
             slot, moff = int(op[4]), int(op[5])
             if mode_bwd and slot >= 0:
                 if kind == S.OP_U1:
-                    w(f"{{ float acc[8] = {{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}}; "
-                      f"u1_coupling<{P.R}, {bits[0]}>(v[0], v[1], acc); warp_accumulate8<{P.NT}>(acc, wacc + {slot}); }}")
+                    nm = P.coup.new(w)
+                    w(f"u1_coupling_h<{P.R}, {bits[0]}>(v[0], v[1], {nm});")
+                    P.coup.push(w, nm, slot, PAT_U1)
                 else:
                     for rr in range(4):
                         w(f"{{ float acc[8] = {{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}}; "
@@ -364,6 +430,7 @@ def generic_smem_bytes(prog, pi: int) -> int:
     b += 4 * (len(pp.phases) * S.PHASE_WORDS + nops * S.OP_WORDS + nsubs * S.SUB_WORDS + 64)
     b += 4 * (((enc["matf"] + 3) & ~3) + ((nw * enc["slotf"] + 3) & ~3))
     b += 8 * 34 + 4 * nw * 32
+    b += 4 * nw * 8  # coupling half-block padding of the specialised kernels
     return (b + 15) & ~15
 
 
@@ -378,6 +445,8 @@ def stage_vectors(prog, pi: int, mode: int) -> int:
 
 def emit_kernel(prog, pi: int, mode: int) -> str:
     P = _Pass(prog, pi)
+    P.coup = _Coup(P)
+    P.slotf = prog.enc[pi]["slotf"]
     nv = 1 if mode == MODE_FWD else 2
     prefetch = stage_vectors(prog, pi, mode) > 0
     nph = len(P.pp.phases)
@@ -393,7 +462,7 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
     w("float2* s_x = reinterpret_cast<float2*>(smem_raw);")
     w(f"float* s_mat = reinterpret_cast<float*>(s_x + {1 << P.M});")
     w(f"float* s_acc = s_mat + {(matf + 3) & ~3};")
-    w(f"double* s_z = reinterpret_cast<double*>(s_acc + {(P.NW * slotf + 3) & ~3});")
+    w(f"double* s_z = reinterpret_cast<double*>(s_acc + {(P.NW * (slotf + 8) + 3) & ~3});")
     w("float* s_zw = reinterpret_cast<float*>(s_z + 34);  // [NW][32] per-warp <Z> partials")
     # next-tile prefetch stage [NV][2^M], natural local order, after the fixed tables so the
     # generic kernel's shared-memory size plus NV x 2^M x 8 B covers it (lsq_program_jit)
@@ -418,14 +487,19 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
             w(f"for (int e = tid; e < {grp.mat_floats}; e += NT) s_mat[{moff} + e] = A.rowtab[((size_t)row * A.nperrow + {ri}) * 32 + e];")
         else:
             w(f"for (int e = tid; e < {grp.mat_floats}; e += NT) s_mat[{moff} + e] = A.gmats[{gid * 32} + e];")
-    w(f"for (int i = tid; i < {P.NW * slotf}; i += NT) s_acc[i] = 0.f;")
+    w(f"for (int i = tid; i < {P.NW * (slotf + 8)}; i += NT) s_acc[i] = 0.f;")
     w("for (int i = tid; i < 34; i += NT) s_z[i] = 0.0;")
     w(f"for (int i = tid; i < {P.NW * 32}; i += NT) s_zw[i] = 0.f;")
     w.ind -= 1
     w("}")
     w("__syncthreads();")
-    w(f"float* wacc = s_acc + warp * {slotf};")
+    # per-warp coupling accumulators: slotf floats + 8 padding floats (zero half-blocks)
+    w(f"float* wacc = s_acc + warp * {slotf + 8};")
     w("(void)wacc;")
+    w("const int lj_ = (tid >> 2) & 3;  // reduce-scatter value index within a half-block")
+    w("const int pu1_ = (0x7431 >> (4 * lj_)) & 15, pdg_ = 2 * lj_ + 1;")
+    w("const bool hi16_ = (tid & 16) != 0;")
+    w("(void)pu1_; (void)pdg_; (void)hi16_;")
     # per-phase thread layout constants
     for k, ph in enumerate(P.pp.phases):
         tp_terms = [f"(((uint32_t)tid >> {j}) & 1u) << {lb}" for j, lb in enumerate(ph.threads)]
@@ -735,6 +809,7 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
             _emit_ops(w, P, k, True, nv)
             if k > 0:
                 _emit_exchange(w, P, k, k - 1, nv)
+        P.coup.flush(w)
 
     def emit_store(k, what):
         if what == "psi":
@@ -792,7 +867,7 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
     if slotf:
         w.block("if (A.part)")
         w(f"double* dst = A.part + (size_t)blockIdx.x * {slotf};")
-        w(f"for (int f = tid; f < {slotf}; f += NT) {{ double s = 0.0; for (int ww = 0; ww < NW; ++ww) s += (double)s_acc[ww * {slotf} + f]; dst[f] = s; }}")
+        w(f"for (int f = tid; f < {slotf}; f += NT) {{ double s = 0.0; for (int ww = 0; ww < NW; ++ww) s += (double)s_acc[ww * {slotf + 8} + f]; dst[f] = s; }}")
         w.end()
     w.block(f"if ((mode == PMODE_TURN || (flags & PF_ZPART)) && A.zpart)")
     w(f"double* dst = A.zpart + (size_t)blockIdx.x * {P.n + 1};")

@@ -283,6 +283,7 @@ size_t smem_bytes(const lsq_program* P, const PassInfo& pi, int NV) {
   b += sizeof(float) * (((pi.matf + 3) & ~3) + ((NW * pi.slotf + 3) & ~3));
   b += sizeof(double) * 34;
   b += sizeof(float) * NW * 32;  // per-warp <Z> / reduction scratch (n + 1 <= 32, M + 1 <= 32)
+  b += sizeof(float) * NW * 8;   // specialised kernels: coupling half-block padding per warp
   return (b + 15) & ~(size_t)15;
 }
 
