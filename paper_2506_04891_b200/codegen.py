@@ -159,6 +159,145 @@ def _emit_const_u(w, P, v, U, regs_bits, dagger):
             _emit_small(w, v, U, q)
 
 
+_PAULI = {
+    "I": np.eye(2, dtype=complex),
+    "X": np.array([[0, 1], [1, 0]], dtype=complex),
+    "Y": np.array([[0, -1j], [1j, 0]], dtype=complex),
+    "Z": np.array([[1, 0], [0, -1]], dtype=complex),
+}
+_STRUCT_CACHE: dict = {}
+
+
+def u1_structure(grp, samples: int = 4):
+    """Structure of a one-qubit group over its parameters (drawn at random; FIXED ones kept):
+
+    * classes[a][b] of U: '0' (always zero), 'r' (real), 'i' (imaginary) or 'c' (complex);
+    * comps: Pauli components P of K = i W that are nonzero for some parameter, W = the
+      anti-Hermitian derivative weight (G_s..G_j+1) dG_j (G_j-1..G_1) U^+ of any free parameter.
+    Only these entries are multiplied and only these components are accumulated."""
+    from .gates import gate_matrix, gate_matrix_derivative
+
+    key = tuple((g.kind, tuple(g.src), tuple(g.fixed)) for g, _ in grp.gates)
+    if key in _STRUCT_CACHE:
+        return _STRUCT_CACHE[key]
+    rng = np.random.default_rng(12345)
+    re_nz = np.zeros((2, 2), bool)
+    im_nz = np.zeros((2, 2), bool)
+    comps = set()
+    for _ in range(samples):
+        mats, ders = [], []
+        for g, _rev in grp.gates:
+            k = GATE_TRAITS[g.kind].param_count
+            if k == 0:
+                mats.append(gate_matrix(g.kind))
+                ders.append([])
+                continue
+            prm = [g.fixed[j] if g.src[j] == S.FIXED_SRC else float(rng.uniform(-3.0, 3.0)) for j in range(k)]
+            mats.append(gate_matrix(g.kind, prm))
+            ders.append([gate_matrix_derivative(g.kind, prm, j) for j in range(k) if g.src[j] != S.FIXED_SRC])
+        U = np.eye(2, dtype=complex)
+        for G in mats:
+            U = G @ U
+        tol = 1e-12 * max(1.0, np.abs(U).max())
+        re_nz |= np.abs(U.real) > tol
+        im_nz |= np.abs(U.imag) > tol
+        for j, dl in enumerate(ders):
+            before = np.eye(2, dtype=complex)
+            for G in mats[:j]:
+                before = G @ before
+            after = np.eye(2, dtype=complex)
+            for G in mats[j + 1:]:
+                after = G @ after
+            for dG in dl:
+                K = 1j * (after @ dG @ before @ U.conj().T)
+                for nm, Pm in _PAULI.items():
+                    if abs(np.trace(Pm @ K)) / 2 > 1e-9:
+                        comps.add(nm)
+    classes = [["0" if not (re_nz[a, b] or im_nz[a, b]) else
+                "c" if (re_nz[a, b] and im_nz[a, b]) else ("r" if re_nz[a, b] else "i")
+                for b in range(2)] for a in range(2)]
+    out = (classes, frozenset(comps))
+    _STRUCT_CACHE[key] = out
+    return out
+
+
+def coupling_layout(comps):
+    """[(component, slot position)] of the anti-Hermitian projected coupling M' (see
+    u1_coupling_h): Z -> M'00.y, X -> M'01.y, Y -> M'10.x; with a trace component the diagonal
+    is kept as A = Im c00 -> M'00.y and B = Im c11 -> M'11.y."""
+    lay = []
+    if "I" in comps:
+        lay += [("A", 1), ("B", 7)]
+    elif "Z" in comps:
+        lay.append(("Z", 1))
+    if "X" in comps:
+        lay.append(("X", 3))
+    if "Y" in comps:
+        lay.append(("Y", 4))
+    return lay
+
+
+# (function, l index, p index) pairs per component: value = sum_pairs (acc.x + acc.y)
+_COMP_TERMS = {
+    "Z": (("_mj", "i", "i"), ("_j", "j", "j")),
+    "X": (("_mj", "i", "j"), ("_mj", "j", "i")),
+    "Y": (("_p", "j", "i"), ("_n", "i", "j")),
+    "A": (("_mj", "i", "i"),),
+    "B": (("_mj", "j", "j"),),
+}
+
+
+def _emit_u1_coupling(w, P, k, slot, comps):
+    lay = coupling_layout(comps)
+    if not lay:
+        return
+    names = [P.coup.new(w) for _ in lay]
+    w("{")
+    w.ind += 1
+    pairs = [(i, i | (1 << k)) for i in range(1 << P.R) if not (i >> k) & 1]
+    for ci, (nm, _pos) in enumerate(lay):
+        acc = None
+        for (i, j) in pairs:
+            idx = {"i": i, "j": j}
+            for fn, li, pi_ in _COMP_TERMS[nm]:
+                a, b = f"v[1][{idx[li]}]", f"v[0][{idx[pi_]}]"
+                acc = f"vm{fn}({a}, {b})" if acc is None else f"vf{fn}({a}, {b}, {acc})"
+        w(f"{{ const float2 t_ = {acc}; {names[ci]} = t_.x + t_.y; }}")
+    w.ind -= 1
+    w("}")
+    used = {pos for _, pos in lay}
+    free = [slot + q for q in range(8) if q not in used]
+    for ci, (nm, pos) in enumerate(lay):
+        P.coup.add(w, names[ci], slot + pos, free)
+
+
+def _emit_u1_struct(w, v, k, R, classes, g, dagger):
+    """U (or U^+) from the table entry g (row-major re, im) on register bit k, emitting only
+    the terms the structure allows: real entry -> one FFMA2, imaginary -> one FFMA2 on i x,
+    complex -> two, zero -> none."""
+    for i in range(1 << R):
+        if (i >> k) & 1:
+            continue
+        j = i | (1 << k)
+        w(f"{{ const float2 x0 = {v}[{i}], x1 = {v}[{j}];")
+        for a, dst in ((0, i), (1, j)):
+            expr = None
+            for b in (0, 1):
+                ra, cb = (b, a) if dagger else (a, b)  # U^+_ab = conj(U_ba)
+                cls = classes[ra][cb]
+                e = 2 * ra + cb
+                re, im = f"{g}[{2 * e}]", f"{g}[{2 * e + 1}]"
+                if cls in ("r", "c"):
+                    expr = f"mx(x{b}, {re})" if expr is None else f"fx(x{b}, {re}, {expr})"
+                if cls in ("i", "c"):
+                    if dagger:
+                        expr = f"mulmix(x{b}, {im})" if expr is None else f"fmix(x{b}, {im}, {expr})"
+                    else:
+                        expr = f"mulix(x{b}, {im})" if expr is None else f"fix(x{b}, {im}, {expr})"
+            w(f"  {v}[{dst}] = {expr if expr else 'make_float2(0.f, 0.f)'};")
+        w("}")
+
+
 def _emit_small(w, v, U, q):
     """Constant complex matrix on packed f32x2: per nonzero coefficient at most two FFMA2
     (real part times x, imaginary part times i*x); zero halves are skipped."""
@@ -172,7 +311,7 @@ def _emit_small(w, v, U, q):
                 if abs(coef) < 1e-15:
                     continue
                 if expr is None:
-                    expr = f"{'mx' if kind == 'x' else 'mix'}(x{c}, {_f(coef)})"
+                    expr = f"{'mx' if kind == 'x' else 'mulix'}(x{c}, {_f(coef)})"
                 else:
                     expr = f"{'fx' if kind == 'x' else 'fix'}(x{c}, {_f(coef)}, {expr})"
         w(f"  {v}[{q[r]}] = {expr if expr else 'make_float2(0.f, 0.f)'};")
@@ -191,73 +330,93 @@ def _src_expr(sw, P, tp_var):
     return "none", None
 
 
-PAT_U1 = (1, 3, 4, 7)    # u1_coupling_h: {Im c00, s, t, Im c11} -> M'00.y, M'01.y, M'10.x, M'11.y
-PAT_DIAG = (1, 3, 5, 7)  # diagonal runs: Im c_e -> M'_e.y (the real parts never reach Re(W M))
-
-
 class _Coup:
-    """Backward couplings as 4-float half-blocks (anti-Hermitian projections, see
-    u1_coupling_h); two half-blocks share one 8-value warp reduce-scatter. A half-block is
-    (array name, slot base, pattern, number of real values); values past `nreal` are zeros
-    that land on the pattern's addresses, so a pairing is refused when such a zero write would
-    hit an address the other half writes in the same instruction."""
+    """Backward coupling values (anti-Hermitian projections, see u1_structure) packed four
+    per half-block; two half-blocks share one 8-value warp reduce-scatter
+    (warp_accumulate8p). Lane l owns value j = (l >> 2) & 3 of half (l >> 4) & 1 and adds it
+    at a per-lane offset: an arithmetic progression o0 + d j when the offsets allow one
+    (padding zeros go to free floats of the same slots or to the 8 padding floats after the
+    slots), else a select chain."""
 
     def __init__(self, P):
         self.P = P
         self.n = 0
-        self.pending = None
+        self.vals = []  # pending (name, offset, free offsets)
+        self.half = None  # pending complete half: (names[4], offsets[4])
 
     def new(self, w):
-        name = f"cp{self.n}_"
+        name = f"cv{self.n}_"
         self.n += 1
-        w(f"float {name}[4];")
+        w(f"float {name};")
         return name
 
-    @staticmethod
-    def _addrs(h):
-        _, base, pat, nreal = h
-        a = [base + o for o in pat]
-        return a[:nreal], a[nreal:]
-
-    def _conflict(self, a, b):
-        ra, za = self._addrs(a)
-        rb, zb = self._addrs(b)
-        return bool(set(za) & set(rb)) or bool(set(zb) & set(ra))
-
-    def push(self, w, name, base, pat, nreal=4):
-        h = (name, base, pat, nreal)
-        a = self.pending
-        self.pending = None
-        if a is not None:
-            if a[3] == 2 and nreal == 2 and a[2] == PAT_DIAG and pat == PAT_DIAG and base == a[1] + 4:
-                nm = self.new(w)
-                w(f"{nm}[0] = {a[0]}[0]; {nm}[1] = {a[0]}[1]; {nm}[2] = {name}[0]; {nm}[3] = {name}[1];")
-                self.pending = (nm, a[1], PAT_DIAG, 4)
-                return
-            if not self._conflict(a, h):
-                self._emit(w, a, h)
-                return
-            self._emit(w, a, None)
-        self.pending = h
+    def add(self, w, name, off, free):
+        self.vals.append((name, off, tuple(free)))
+        if len(self.vals) == 4:
+            self._close(w)
 
     def flush(self, w):
-        if self.pending is not None:
-            a = self.pending
-            self.pending = None
-            self._emit(w, a, None)
+        if self.vals:
+            self._close(w)
+        if self.half is not None:
+            h, self.half = self.half, None
+            self._emit(w, h, None)
+
+    def _close(self, w):
+        vals, self.vals = self.vals, []
+        h = self._layout(vals)
+        if self.half is None:
+            self.half = h
+        else:
+            a, self.half = self.half, None
+            self._emit(w, a, h)
+
+    def _layout(self, vals):
+        """(names[4], offsets[4], offset expression) of one half-block."""
+        P = self.P
+        reals = {off: nm for nm, off, _ in vals}
+        nz = 4 - len(vals)
+        pad = [P.slotf + q for q in range(8)]
+        cand = sorted({f for _, _, fr in vals for f in fr} - set(reals)) + pad
+        best = None
+        if P.NT >= 32:
+            for o0 in sorted(set(reals) | set(cand)):
+                for d in (1, 2, 3, 4, 8, -1, -2, -4, -8):
+                    offs = [o0 + d * q for q in range(4)]
+                    if not set(reals) <= set(offs):
+                        continue
+                    zs = [o for o in offs if o not in reals]
+                    if len(zs) == nz and all(z in cand for z in zs):
+                        best = (offs, f"{o0} + {d} * lj_" if d != 1 else f"{o0} + lj_")
+                        break
+                if best:
+                    break
+            if best is None:
+                for base in sorted({o - p for o in reals for p in (1, 3, 4, 7)}):
+                    offs = [base + p for p in (1, 3, 4, 7)]
+                    zs = [o for o in offs if o not in reals]
+                    if set(reals) <= set(offs) and len(zs) == nz and all(z in cand for z in zs):
+                        best = (offs, f"{base} + pu1_")
+                        break
+        if best is None:
+            offs = list(reals) + pad[:nz]
+            sel = f"(lj_ & 2 ? (lj_ & 1 ? {offs[3]} : {offs[2]}) : (lj_ & 1 ? {offs[1]} : {offs[0]}))"
+            best = (offs, sel)
+        offs, expr = best
+        names = [reals.get(o, "0.f") for o in offs]
+        return names, offs, expr
 
     def _emit(self, w, a, b):
         P = self.P
-        vals = [f"{a[0]}[{k}]" for k in range(4)] + ([f"{b[0]}[{k}]" for k in range(4)] if b else ["0.f"] * 4)
+        vals = list(a[0]) + (list(b[0]) if b else ["0.f"] * 4)
         init = f"float a8_[8] = {{{', '.join(vals)}}};"
         if P.NT >= 32:
-            bb = b if b is not None else (None, P.slotf, PAT_DIAG, 0)  # zero half -> padding
-            pv = {PAT_U1: "pu1_", PAT_DIAG: "pdg_"}
-            w(f"{{ {init} warp_accumulate8p<NT>(a8_, wacc + (hi16_ ? {bb[1]} + {pv[bb[2]]} : {a[1]} + {pv[a[2]]})); }}")
+            eb = b[2] if b else f"{P.slotf} + lj_"
+            w(f"{{ {init} warp_accumulate8p<NT>(a8_, wacc + (hi16_ ? {eb} : {a[2]})); }}")
         else:
-            adds = [f"wacc[{a[1] + a[2][k]}] += a8_[{k}];" for k in range(a[3])]
-            if b is not None:
-                adds += [f"wacc[{b[1] + b[2][k]}] += a8_[{4 + k}];" for k in range(b[3])]
+            adds = [f"wacc[{o}] += a8_[{q}];" for q, (nm, o) in enumerate(zip(a[0], a[1])) if nm != "0.f"]
+            if b:
+                adds += [f"wacc[{o}] += a8_[{4 + q}];" for q, (nm, o) in enumerate(zip(b[0], b[1])) if nm != "0.f"]
             w(f"{{ {init} warp_sum<NT, 8>(a8_); if ((tid & 31) == 0) {{ {' '.join(adds)} }} }}")
 
 
@@ -267,7 +426,7 @@ def _emit_drun(w, P, op, ph_idx, mode_bwd, nv):
     R = P.R
     # couplings (backward, before un-applying: conj(l) p is phase invariant)
     if mode_bwd and any(int(s[4]) >= 0 for s in subs):
-        names = {si: P.coup.new(w) for si, s in enumerate(subs) if int(s[4]) >= 0}
+        names = {si: [P.coup.new(w) for _ in range(1 << int(s[5]))] for si, s in enumerate(subs) if int(s[4]) >= 0}
         w("{")
         w.ind += 1
         for i in range(P.NR):
@@ -289,7 +448,7 @@ def _emit_drun(w, P, op, ph_idx, mode_bwd, nv):
                     b = ((i >> eb) & 1) if kb == "reg" else None
                     e = (a, b)
                 terms.setdefault(e, []).append(i)
-            w(" ".join(f"{nm}[{k}] = {'-0.f' if k < (1 << ar) else '0.f'};" for k in range(4)))
+            w(" ".join(f"{nm[k]} = -0.f;" for k in range(1 << ar)))
             for e, idxs in terms.items():
                 sy = " + ".join(f"c{i}" for i in idxs)
                 if ar == 1:
@@ -302,17 +461,21 @@ def _emit_drun(w, P, op, ph_idx, mode_bwd, nv):
                         b_e = str(e[1]) if e[1] is not None else eb
                         ix = f"(2 * ({a_e}) + ({b_e}))"
                 if ix.isdigit():
-                    w(f"{nm}[{int(ix)}] += {sy};")
+                    w(f"{nm[int(ix)]} += {sy};")
                 else:
                     w(f"{{ const int e_ = {ix}; const float sy_ = {sy};")
                     for ee in range(1 << ar):
-                        w(f"  {nm}[{ee}] += e_ == {ee} ? sy_ : 0.f;")
+                        w(f"  {nm[ee]} += e_ == {ee} ? sy_ : 0.f;")
                     w("}")
         w.ind -= 1
         w("}")
         for si, s in enumerate(subs):
-            if int(s[4]) >= 0:
-                P.coup.push(w, names[si], int(s[4]), PAT_DIAG, 1 << int(s[5]))
+            slot = int(s[4])
+            if slot >= 0:
+                ne = 1 << int(s[5])
+                free = [slot + 2 * e for e in range(ne)]
+                for e in range(ne):
+                    P.coup.add(w, names[si][e], slot + 2 * e + 1, free)
     # phases
     w("{")
     w.ind += 1
@@ -374,9 +537,7 @@ def _emit_ops(w, P, ph_idx, mode_bwd, nv):
             slot, moff = int(op[4]), int(op[5])
             if mode_bwd and slot >= 0:
                 if kind == S.OP_U1:
-                    nm = P.coup.new(w)
-                    w(f"u1_coupling_h<{P.R}, {bits[0]}>(v[0], v[1], {nm});")
-                    P.coup.push(w, nm, slot, PAT_U1)
+                    _emit_u1_coupling(w, P, bits[0], slot, u1_structure(grp)[1])
                 else:
                     for rr in range(4):
                         w(f"{{ float acc[8] = {{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}}; "
@@ -387,14 +548,11 @@ def _emit_ops(w, P, ph_idx, mode_bwd, nv):
                 for q in range(nv):
                     _emit_const_u(w, P, f"v[{q}]", U, bits, mode_bwd)
             elif kind == S.OP_U1:
-                if mode_bwd:
-                    w(f"{{ const float* g = s_mat + {moff};")
-                    for q in range(nv):
-                        w(f"  u1_apply_dag<{P.R}, {bits[0]}>(v[{q}], g);")
-                    w("}")
-                else:
-                    w(f"{{ float m[8]; for (int e = 0; e < 8; ++e) m[e] = s_mat[{moff} + e]; "
-                      f"u1_apply<{P.R}, {bits[0]}>(v[0], m); }}")
+                classes = u1_structure(grp)[0]
+                w(f"{{ const float* g_ = s_mat + {moff};")
+                for q in range(nv if mode_bwd else 1):
+                    _emit_u1_struct(w, f"v[{q}]", bits[0], P.R, classes, "g_", mode_bwd)
+                w("}")
             else:
                 if mode_bwd:
                     for q in range(nv):
