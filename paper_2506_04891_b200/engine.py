@@ -127,7 +127,7 @@ class Engine:
     """A circuit compiled for the device; the object behind the drop-in API."""
 
     def __init__(self, circuit, M: int | None = None, R: int | None = None, device=None, jit=None,
-                 isolate=(), prefix=None, fold=None):
+                 isolate=(), prefix=None, fold=None, split=None):
         self.device = torch.device(device if device is not None else "cuda")
         if self.device.type != "cuda":
             raise ValueError("the engine runs on CUDA devices only")
@@ -152,7 +152,12 @@ class Engine:
             fold = bool(prefix) and os.environ.get("LSQ_FOLD", "1") != "0"
         if fold and not jit:
             raise ValueError("the folded observable needs the specialised (JIT) kernels")
-        self.program = compile_circuit(circuit, M=M, R=R, isolate=isolate, prefix=prefix, fold=fold)
+        # diagonal gates split out of one-qubit groups when the remainder is cheaper (JIT only:
+        # the structure-aware apply is what makes the remainder cheaper)
+        if split is None:
+            split = jit and os.environ.get("LSQ_SPLIT", "1") != "0"
+        self.program = compile_circuit(circuit, M=M, R=R, isolate=isolate, prefix=prefix, fold=fold,
+                                       split=split)
         self.prefix = bool(self.program.prefix) or bool(self.program.obs)
         self.native = NativeProgram(self.program, self.device)
         if jit:

@@ -261,6 +261,36 @@ def fuse_groups(gates: list[GateRef]) -> list[Group]:
     return groups
 
 
+def _apply_cost(grp: Group) -> int:
+    """Packed-FMA count per amplitude pair of a one-qubit group in the specialised kernels."""
+    from .codegen import u1_structure
+
+    cls = u1_structure(grp)[0]
+    return sum({"0": 0, "r": 1, "i": 1, "c": 2}[c] for row in cls for c in row)
+
+
+def split_diagonal(groups: list[Group], keep=()) -> list[Group]:
+    """Split one-qubit groups into runs of diagonal and non-diagonal gates when the
+    non-diagonal remainder is cheaper to apply (RZ.RY -> real RY + a phase in a diagonal
+    run). The diagonal parts then join diagonal runs, where a wire that is not a register bit
+    costs no per-amplitude work. Groups in `keep` (product-state prefix) stay whole."""
+    out: list[Group] = []
+    for g in groups:
+        runs = []
+        for gr in g.gates:
+            if runs and runs[-1][0].diag == gr[0].diag:
+                runs[-1].append(gr)
+            else:
+                runs.append([gr[0], gr])
+        parts = [r[1:] for r in runs]
+        split = (g.gid not in keep and g.arity == 1 and len(parts) > 1
+                 and sum(_apply_cost(Group(0, g.wires, p)) for p in parts if not p[0][0].diag)
+                 < _apply_cost(g))
+        for p in (parts if split else [g.gates]):
+            out.append(Group(len(out), g.wires, list(p), g.prefix, g.trailing))
+    return out
+
+
 def group_preds(groups: list[Group]) -> list[set]:
     """Dependency sets: two groups sharing a wire are ordered unless both are diagonal."""
     preds = [set() for _ in groups]
@@ -443,6 +473,9 @@ def schedule_phases(pp: PassPlan, groups, preds, n: int, R: int) -> None:
                 opset.add(gid)
         if not ops and not first:
             raise RuntimeError("phase scheduler made no progress")
+        ops = _defer_diagonal(ops, regs, remaining, groups,
+                              lambda w: pp.local_of_phys.get(n - 1 - w, -1))
+        opset = set(ops)
         phases.append([regs, ops])
         done |= opset
         remaining = [g for g in remaining if g not in opset]
@@ -455,6 +488,7 @@ def schedule_phases(pp: PassPlan, groups, preds, n: int, R: int) -> None:
         phases.insert(0, [set(), []])
     out = []
     for i, (regs, ops) in enumerate(phases):
+        ops = _sink_diagonal(ops, groups)
         coalesced = coal and (i == 0 or i == len(phases) - 1)
         regs = sorted(regs)
         pool = [b for b in range(M) if b not in regs and not (coalesced and b in low)]
@@ -469,6 +503,48 @@ def schedule_phases(pp: PassPlan, groups, preds, n: int, R: int) -> None:
         out.append(PhasePlan(regs, threads, ops))
     pp.phases = out
     pp.R = R
+
+
+def _defer_diagonal(ops, regs, remaining, groups, loc):
+    """Drop from this phase the diagonal groups that touch one of its register bits when
+    nothing later in the phase needs them and a later phase exists: applied in a phase where
+    their wires are thread or tile bits, their phase is one value per thread."""
+    nd_left = any(not groups[g].diag for g in remaining if g not in ops)
+    if not nd_left:
+        return ops
+    keep = []
+    for idx, gid in enumerate(ops):
+        g = groups[gid]
+        if g.diag and {loc(w) for w in g.wires} & regs:
+            later = ops[idx + 1:]
+            if not any(not groups[x].diag and set(groups[x].wires) & set(g.wires) for x in later):
+                continue
+        keep.append(gid)
+    return keep
+
+
+def _sink_diagonal(ops, groups):
+    """Move every diagonal group as late as its wires allow (before the next non-diagonal
+    group sharing a wire, else to the end) so diagonal groups form long runs (one DRUN)."""
+    nd = [g for g in ops if not groups[g].diag]
+    slots: dict = {}  # index into nd (or len(nd)) -> diagonal groups placed before it
+    for idx, gid in enumerate(ops):
+        g = groups[gid]
+        if not g.diag:
+            continue
+        pos = len(nd)
+        seen_nd = sum(1 for x in ops[:idx] if not groups[x].diag)
+        for k in range(seen_nd, len(nd)):
+            if set(groups[nd[k]].wires) & set(g.wires):
+                pos = k
+                break
+        slots.setdefault(pos, []).append(gid)
+    out = []
+    for k in range(len(nd) + 1):
+        out += slots.get(k, [])
+        if k < len(nd):
+            out.append(nd[k])
+    return out
 
 
 # ----------------------------------------------------------------------------- program
@@ -551,7 +627,7 @@ def observable_masks(perms, n: int):
 
 
 def compile_circuit(circuit, M: int | None = None, R: int | None = None, isolate=(),
-                    prefix: bool = False, fold: bool = False) -> Program:
+                    prefix: bool = False, fold: bool = False, split: bool = False) -> Program:
     """Compile a (reference-compatible) circuit into a pass program.
 
     `isolate`: layer indices executed with pass boundaries of their own (planner variant
@@ -579,6 +655,8 @@ def compile_circuit(circuit, M: int | None = None, R: int | None = None, isolate
     obs = None
     for si, seg in enumerate(segs):
         grp = fuse_groups(seg)
+        if split:
+            grp = split_diagonal(grp, set(prefix_groups(grp).values()) if (prefix and si == 0) else ())
         preds = group_preds(grp)
         skip = set()
         if prefix and si == 0:

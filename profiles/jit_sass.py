@@ -14,6 +14,7 @@ ap.add_argument("R", type=int, nargs="?", default=4)
 ap.add_argument("--dump", default=None)
 ap.add_argument("--only", default=None)
 ap.add_argument("--no-prefix", action="store_true")
+ap.add_argument("--no-split", action="store_true")
 a = ap.parse_args()
 
 lib = ctypes.CDLL(os.path.realpath("/usr/local/cuda/lib64/libnvrtc.so.12"))
@@ -39,7 +40,8 @@ def compile_cubin(src):
 
 wl = make_workload(a.cfg)
 pre = not a.no_prefix
-prog = compile_circuit(wl.circuit, M=a.M, R=a.R, prefix=pre, fold=pre)
+prog = compile_circuit(wl.circuit, M=a.M, R=a.R, prefix=pre, fold=pre, split=not a.no_split)
+print(len(prog.passes), "passes")
 only = set(a.only.split(",")) if a.only else None
 tot = collections.Counter()
 for pi, mode, name, src, sv in codegen.generate_kernels(prog):

@@ -128,3 +128,38 @@ def test_random_circuits_folding(c):
     prog = S.compile_circuit(circ, M=4, R=2, prefix=True, fold=True)
     res = Emulator(prog).gradient(gold[f"c{c}_theta"], gold[f"c{c}_x"], 3, gold[f"c{c}_w"])
     _cmp(res, {k[len(f"c{c}_"):]: v for k, v in gold.items() if k.startswith(f"c{c}_")}, atol=1e-8)
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("M,R", [(6, 2), (5, 3), (4, 2)])
+def test_split_diagonal(cfg, M, R):
+    """Diagonal gates split out of one-qubit groups (RZ.RY -> RY + diagonal run), deferred off
+    register bits and sunk into runs: same results."""
+    wl = make_workload(cfg, n=6, batch=3)
+    prog = S.compile_circuit(wl.circuit, M=M, R=R, prefix=True, fold=True, split=True)
+    if cfg == 2:  # RY.RZ groups outside the prefix are split
+        assert any(g.diag and g.arity == 1 and not g.prefix for g in prog.groups)
+    res = Emulator(prog).gradient(wl.theta, wl.x, 3, wl.weights)
+    ref = orc.gradient(wl.circuit, wl.theta, wl.x, batch=3, weights=wl.weights)
+    _cmp(res, ref, atol=1e-8)
+
+
+@pytest.mark.parametrize("c", range(6))
+def test_random_circuits_split(c):
+    gold = load_golden("random_circuits")
+    circ = rebuild_random(gold[f"c{c}_spec"])
+    prog = S.compile_circuit(circ, M=4, R=2, prefix=True, fold=True, split=True)
+    res = Emulator(prog).gradient(gold[f"c{c}_theta"], gold[f"c{c}_x"], 3, gold[f"c{c}_w"])
+    _cmp(res, {k[len(f"c{c}_"):]: v for k, v in gold.items() if k.startswith(f"c{c}_")}, atol=1e-8)
+
+
+def test_diagonal_runs_are_sunk():
+    """After sinking, no phase has two diagonal runs separated only by groups on other wires."""
+    wl = make_workload(2, n=16, batch=1)
+    prog = S.compile_circuit(wl.circuit, M=12, R=4, prefix=True, fold=True, split=True)
+    for pp in prog.passes:
+        for ph in pp.phases:
+            kinds = [prog.groups[g].diag for g in ph.ops]
+            runs = sum(1 for i, d in enumerate(kinds) if d and (i == 0 or not kinds[i - 1]))
+            nd_after = [i for i, d in enumerate(kinds) if not d]
+            assert runs <= max(1, len(nd_after)), (kinds,)
