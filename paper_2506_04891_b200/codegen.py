@@ -130,11 +130,21 @@ class _W:
         self("}" + tail)
 
 
-def _group_const_matrix(grp):
-    """Compile-time matrix of a group whose parameters are all FIXED (or absent)."""
+def phase_normalized(U):
+    """U times the global phase that makes its largest entry real positive (SX -> X90 with
+    real diagonal and imaginary off-diagonal entries)."""
+    k = np.unravel_index(np.argmax(np.abs(U)), U.shape)
+    return U * np.exp(-1j * np.angle(U[k]))
+
+
+def _group_const_matrix(grp, drop_phase=False):
+    """Compile-time matrix of a group whose parameters are all FIXED (or absent). Gradient
+    programs (folded observable, no state returned) drop its global phase: <Z_q> and every
+    coupling conj(lam) psi are invariant under a common phase of psi and lam = O psi."""
     if any(s != S.FIXED_SRC for g, _ in grp.gates for s in g.src):
         return None
-    return S.group_matrix_host(grp)
+    U = S.group_matrix_host(grp)
+    return phase_normalized(U) if drop_phase else U
 
 
 def _emit_const_u(w, P, v, U, regs_bits, dagger):
@@ -543,7 +553,7 @@ def _emit_ops(w, P, ph_idx, mode_bwd, nv):
                         w(f"{{ float acc[8] = {{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}}; "
                           f"u2_coupling_row<{P.R}, {bits[0]}, {bits[1]}, {rr}>(v[0], v[1], acc); "
                           f"warp_accumulate8<{P.NT}>(acc, wacc + {slot + 8 * rr}); }}")
-            U = _group_const_matrix(grp)
+            U = _group_const_matrix(grp, P.drop_phase)
             if U is not None:
                 for q in range(nv):
                     _emit_const_u(w, P, f"v[{q}]", U, bits, mode_bwd)
@@ -604,6 +614,7 @@ def stage_vectors(prog, pi: int, mode: int) -> int:
 def emit_kernel(prog, pi: int, mode: int) -> str:
     P = _Pass(prog, pi)
     P.coup = _Coup(P)
+    P.drop_phase = bool(getattr(prog, "drop_phase", False))
     P.slotf = prog.enc[pi]["slotf"]
     nv = 1 if mode == MODE_FWD else 2
     prefetch = stage_vectors(prog, pi, mode) > 0
@@ -625,7 +636,11 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
     # next-tile prefetch stage [NV][2^M], natural local order, after the fixed tables so the
     # generic kernel's shared-memory size plus NV x 2^M x 8 B covers it (lsq_program_jit)
     use_prefix = bool(getattr(prog, "prefix", None)) and pi == 0
-    w(f"float2* s_stage = reinterpret_cast<float2*>((reinterpret_cast<size_t>(s_zw + {P.NW * 32}) + 15) & ~(size_t)15);")
+    # byte offset of the stage as a constant so the compiler keeps the shared window (LDS, not
+    # generic LD) for the stage reads
+    off = (8 << P.M) + 4 * ((matf + 3) & ~3) + 4 * ((P.NW * (slotf + 8) + 3) & ~3) + 8 * 34 + 4 * P.NW * 32
+    off = (off + 15) & ~15
+    w(f"float2* s_stage = reinterpret_cast<float2*>(smem_raw + {off});")
     # the prefix vectors live in the first 8*n bytes of the exchange buffer's tail region: use a
     # dedicated register-free path -- they are read from global (L1-cached, 16 B per wire)
     w("const int tid = threadIdx.x, warp = tid >> 5;")

@@ -261,15 +261,22 @@ def fuse_groups(gates: list[GateRef]) -> list[Group]:
     return groups
 
 
-def _apply_cost(grp: Group) -> int:
+def _apply_cost(grp: Group, drop_phase: bool = False) -> int:
     """Packed-FMA count per amplitude pair of a one-qubit group in the specialised kernels."""
-    from .codegen import u1_structure
+    from .codegen import phase_normalized, u1_structure
 
-    cls = u1_structure(grp)[0]
+    if drop_phase and not grp.needs_grad and not any(GATE_TRAITS[g.kind].param_count and
+                                                     any(s != FIXED_SRC for s in g.src)
+                                                     for g, _ in grp.gates):
+        U = phase_normalized(group_matrix_host(grp))
+        cls = [["0" if abs(z) < 1e-12 else "c" if abs(z.real) > 1e-12 and abs(z.imag) > 1e-12
+                else "r" if abs(z.real) > 1e-12 else "i" for z in row] for row in U]
+    else:
+        cls = u1_structure(grp)[0]
     return sum({"0": 0, "r": 1, "i": 1, "c": 2}[c] for row in cls for c in row)
 
 
-def split_diagonal(groups: list[Group], keep=()) -> list[Group]:
+def split_diagonal(groups: list[Group], keep=(), drop_phase: bool = False) -> list[Group]:
     """Split one-qubit groups into runs of diagonal and non-diagonal gates when the
     non-diagonal remainder is cheaper to apply (RZ.RY -> real RY + a phase in a diagonal
     run). The diagonal parts then join diagonal runs, where a wire that is not a register bit
@@ -283,9 +290,12 @@ def split_diagonal(groups: list[Group], keep=()) -> list[Group]:
             else:
                 runs.append([gr[0], gr])
         parts = [r[1:] for r in runs]
+        # a diagonal part followed by a non-diagonal one runs where its wire is a register bit
+        # (one complex phase per amplitude, charged 4); trailing diagonal parts are deferred
+        cost = sum(_apply_cost(Group(0, g.wires, p), drop_phase) if not p[0][0].diag else
+                   (4 if k < len(parts) - 1 else 0) for k, p in enumerate(parts))
         split = (g.gid not in keep and g.arity == 1 and len(parts) > 1
-                 and sum(_apply_cost(Group(0, g.wires, p)) for p in parts if not p[0][0].diag)
-                 < _apply_cost(g))
+                 and cost < _apply_cost(g, drop_phase))
         for p in (parts if split else [g.gates]):
             out.append(Group(len(out), g.wires, list(p), g.prefix, g.trailing))
     return out
@@ -656,7 +666,8 @@ def compile_circuit(circuit, M: int | None = None, R: int | None = None, isolate
     for si, seg in enumerate(segs):
         grp = fuse_groups(seg)
         if split:
-            grp = split_diagonal(grp, set(prefix_groups(grp).values()) if (prefix and si == 0) else ())
+            grp = split_diagonal(grp, set(prefix_groups(grp).values()) if (prefix and si == 0) else (),
+                                 drop_phase=fold)
         preds = group_preds(grp)
         skip = set()
         if prefix and si == 0:
@@ -708,6 +719,7 @@ def compile_circuit(circuit, M: int | None = None, R: int | None = None, isolate
     prog.isolate = tuple(sorted(iso))
     prog.prefix = {w: gid for w, gid in pre.items()}
     prog.obs = obs
+    prog.drop_phase = bool(fold)  # gradient program: global phases of constant groups dropped
     encode(prog)
     return prog
 
