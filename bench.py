@@ -266,6 +266,17 @@ def run_ours(args, world, rank, local):
     wl, r0, r1, gbatch, scaling = _workload_rows(cfg, world, rank, args.batch)
     b = r1 - r0
     n = wl.n
+    # tile exponent: measured by the planner on a bounded row sample (plan build excluded from
+    # the timed region, as the reference's bench does), unless --M is given
+    plan, tile_choice = None, None
+    if args.M is None:
+        from paper_2506_04891_b200.planner import Objective, choose_tile_bits, plan_for_tile_bits
+
+        prow = max(1, min(b, (2 << 30) // (8 << wl.n)))
+        M_best, st = choose_tile_bits(wl.circuit, prow, Objective.FORWARD_BACKWARD, device=dev)
+        tile_choice = {"rows": prow, "ms": {str(m): round(v.mean_seconds * 1e3, 3) for m, v in st.items()}}
+        plan = plan_for_tile_bits(wl.circuit, b, M_best)
+        args.M = M_best
     eng = Engine(wl.circuit, device=dev, M=args.M, R=args.R)
     theta = torch.as_tensor(wl.theta, device=dev)
     x = torch.as_tensor(wl.x[r0:r1], device=dev)
@@ -365,11 +376,11 @@ def run_ours(args, world, rank, local):
     h2d = wl.theta.nbytes + x_host.nbytes + wl.weights.nbytes
     res = None
     for _ in range(1):
-        res = gradient(wl.circuit, wl.theta, x_host, batch=b, weights=wl.weights, device=dev)
+        res = gradient(wl.circuit, wl.theta, x_host, batch=b, weights=wl.weights, device=dev, plan=plan)
     barrier()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        res = gradient(wl.circuit, wl.theta, x_host, batch=b, weights=wl.weights, device=dev)
+        res = gradient(wl.circuit, wl.theta, x_host, batch=b, weights=wl.weights, device=dev, plan=plan)
         if world > 1:
             import torch.distributed as dist
 
@@ -410,6 +421,7 @@ def run_ours(args, world, rank, local):
                    "rows_per_gpu": b, "micro_batch": mb, "adjoint": eng.last_adjoint,
                    "parallelism": f"dp{world}",
                    "passes": len(eng.program.passes), "tile_bits": eng.program.passes[0].M,
+                   "tile_bits_choice": tile_choice,
                    "cuda_graph": gstep.graph is not None,
                    "reg_bits": eng.program.passes[0].R, "variant": eng.variant,
                    "l2": f"working set {2 * b * (8 << n) / 2**20:.0f} MiB (psi+lambda) vs 126 MB L2"

@@ -789,7 +789,16 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
 
     def emit_prefix_lambda(k):
         """Lambda_w(a) = sum_{j: bit_w(j)=a} conj(lam_j) prod_{w' != w} v_w'(bit_w'(j)) for every
-        prefix wire with a coupling slot, at the prefix boundary (end of the last adjoint pass)."""
+        prefix wire with a coupling slot, at the prefix boundary (end of the last adjoint pass).
+
+        With S = sum_i conj(lam_i) Kr_i over the thread's registers (Kr: Kronecker product of
+        the register wires' factors), C_thr / C_nl the products of the thread-bit / tile-bit
+        wires' factors:
+        * tile-bit wire t: Lambda_t(b_t) += NLO_t * sum_warp (C_thr S), NLO_t = prod over the
+          other tile-bit wires (one complex per warp and tile, lane 0);
+        * thread-bit wire t: C_nl * C_thr/t * S per thread (leave-one-out with a running
+          suffix: O(#thread bits) registers);
+        * register wire k: C_nl * C_thr * sum_{b_k(i)=a} conj(lam_i) prod_{k' != k} v_k'."""
         slots = {}
         pre = prog.prefix
         for wire, gid in pre.items():
@@ -800,46 +809,81 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
             return
         ph = P.pp.phases[k]
         reg_w = [wire_of_local(ph.regs[kk]) for kk in range(P.R)]
-        consts = [(wire_of_local(lb), f"(tp{k} >> {lb}) & 1u") for lb in ph.threads]
-        consts += [(P.n - 1 - p, f"(int)((tbase >> {p}) & 1ull)") for p in P.nbit]
+        thr = [(wire_of_local(lb), f"(tp{k} >> {lb}) & 1u") for lb in ph.threads]
+        nl = [(P.n - 1 - p, f"(int)((tbase >> {p}) & 1ull)") for p in P.nbit]
+        nt = len(thr)
         w("{")
         w.ind += 1
-        # constant factors, prefix / suffix products for leave-one-out
-        nc = len(consts)
-        for ci, (wr, ix) in enumerate(consts):
+        # thread-bit factors, prefix products
+        for ci, (wr, ix) in enumerate(thr):
             w(f"const float2 f{ci} = {pv(wr, ix)};")
         w("float2 pre0 = make_float2(1.f, 0.f);")
-        for ci in range(nc):
+        for ci in range(nt):
             w(f"const float2 pre{ci + 1} = cm(f{ci}.x, f{ci}.y, pre{ci});")
-        w(f"const float2 suf{nc} = make_float2(1.f, 0.f);")
-        for ci in range(nc - 1, -1, -1):
-            w(f"const float2 suf{ci} = cm(f{ci}.x, f{ci}.y, suf{ci + 1});")
         # register Kronecker product Kr and S = sum conj(lam) Kr
+        w(f"float2 S_ = make_float2(0.f, 0.f);")
+        w("{")
         w(f"float2 kr[{P.NR}]; kr[0] = make_float2(1.f, 0.f);")
         for kk in range(P.R):
             w(f"{{ const float2 a0 = {pv(reg_w[kk], '0')}, a1 = {pv(reg_w[kk], '1')};")
             for i in range(1 << kk):
                 w(f"  kr[{i | (1 << kk)}] = cm(a1.x, a1.y, kr[{i}]); kr[{i}] = cm(a0.x, a0.y, kr[{i}]);")
             w("}")
-        w("float2 S_ = make_float2(0.f, 0.f);")
         for i in range(P.NR):
             w(f"S_ = cjfma(v[1][{i}], kr[{i}], S_);")
-        # constant-factor wires: Lambda_t(b_t) += C_{not t} * S
-        for ci, (wr, ix) in enumerate(consts):
-            if wr not in slots:
-                continue
-            w(f"{{ const float2 cn = cm(suf{ci + 1}.x, suf{ci + 1}.y, pre{ci}); const float2 val = cm(cn.x, cn.y, S_);")
-            w(f"  const int b_ = {ix}; float acc[4] = {{b_ ? 0.f : val.x, b_ ? 0.f : val.y, b_ ? val.x : 0.f, b_ ? val.y : 0.f}};")
-            w(f"  warp_accumulate<NT, 4>(acc, wacc + {slots[wr]}); }}")
-        # register wires: Lambda_k(a) = C_all * sum_{b_k(i)=a} conj(lam_i) prod_{k' != k} v_k'(b_k'(i))
+        w("}")
+        w(f"const float2 Q_ = cm(pre{nt}.x, pre{nt}.y, S_);  // C_thr S")
+        # tile-bit wires: warp sum of Q, lane 0 scales by the leave-one-out tile products
+        w("float2 cnl_ = make_float2(1.f, 0.f);")
+        if nl:
+            w("{ float q_[2] = {Q_.x, Q_.y}; warp_sum<NT, 2>(q_);")
+            w.block("if ((tid & 31) == 0)")
+            for ci, (wr, ix) in enumerate(nl):
+                w(f"const float2 g{ci} = {pv(wr, ix)};")
+            w("float2 run_ = make_float2(1.f, 0.f);")
+            w(f"float2 gp_[{len(nl) + 1}]; gp_[0] = run_;")
+            for ci in range(len(nl)):
+                w(f"gp_[{ci + 1}] = cm(g{ci}.x, g{ci}.y, gp_[{ci}]);")
+            for ci in range(len(nl) - 1, -1, -1):
+                wr, ix = nl[ci]
+                if wr in slots:
+                    w(f"{{ const float2 lo = cm(run_.x, run_.y, gp_[{ci}]); const float2 val = cm(lo.x, lo.y, make_float2(q_[0], q_[1]));")
+                    w(f"  const int b_ = {ix}; wacc[{slots[wr]} + 2 * b_] += val.x; wacc[{slots[wr]} + 2 * b_ + 1] += val.y; }}")
+                w(f"run_ = cm(g{ci}.x, g{ci}.y, run_);")
+            w(f"cnl_ = gp_[{len(nl)}];")
+            w.end()
+            w("const unsigned FULL_ = 0xffffffffu;" if P.NT >= 32 else f"const unsigned FULL_ = {(1 << P.NT) - 1}u;")
+            w("cnl_.x = __shfl_sync(FULL_, cnl_.x, 0); cnl_.y = __shfl_sync(FULL_, cnl_.y, 0); }")
+        # thread-bit wires: running suffix over the thread factors
+        names = {}
+        for ci, (wr, _) in enumerate(thr):
+            if wr in slots:
+                names[ci] = [P.coup.new(w) for _ in range(4)]
+        regn = {}
         for kk in range(P.R):
-            wr = reg_w[kk]
-            if wr not in slots:
+            if reg_w[kk] in slots:
+                regn[kk] = [P.coup.new(w) for _ in range(4)]
+        w("{")
+        w.ind += 1
+        w("const float2 cs_ = cm(cnl_.x, cnl_.y, S_);  // C_nl S")
+        w("float2 suf_ = make_float2(1.f, 0.f);")
+        for ci in range(nt - 1, -1, -1):
+            wr, ix = thr[ci]
+            if ci in names:
+                nm = names[ci]
+                w(f"{{ const float2 lo = cm(suf_.x, suf_.y, pre{ci}); const float2 val = cm(lo.x, lo.y, cs_); const bool b_ = {ix};")
+                w(f"  {nm[0]} = b_ ? 0.f : val.x; {nm[1]} = b_ ? 0.f : val.y; {nm[2]} = b_ ? val.x : 0.f; {nm[3]} = b_ ? val.y : 0.f; }}")
+            if ci > 0:
+                w(f"suf_ = cm(f{ci}.x, f{ci}.y, suf_);")
+        # register wires
+        w(f"const float2 call_ = cm(cnl_.x, cnl_.y, pre{nt});")
+        for kk in range(P.R):
+            if kk not in regn:
                 continue
             others = [k2 for k2 in range(P.R) if k2 != kk]
             w("{")
             w.ind += 1
-            w(f"float2 ko[{1 << (P.R - 1)}]; ko[0] = pre{nc};")
+            w(f"float2 ko[{1 << (P.R - 1)}]; ko[0] = call_;")
             for t2, k2 in enumerate(others):
                 w(f"{{ const float2 a0 = {pv(reg_w[k2], '0')}, a1 = {pv(reg_w[k2], '1')};")
                 for i in range(1 << t2):
@@ -847,13 +891,24 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
                 w("}")
             w("float2 L0 = make_float2(0.f, 0.f), L1 = make_float2(0.f, 0.f);")
             for i in range(P.NR):
-                # index into ko: bits of i without bit kk, in the order of `others`
                 oi = sum(((i >> k2) & 1) << t2 for t2, k2 in enumerate(others))
                 tgt = "L1" if (i >> kk) & 1 else "L0"
                 w(f"{tgt} = cjfma(v[1][{i}], ko[{oi}], {tgt});")
-            w(f"float acc[4] = {{L0.x, L0.y, L1.x, L1.y}}; warp_accumulate<NT, 4>(acc, wacc + {slots[wr]});")
+            nm = regn[kk]
+            w(f"{nm[0]} = L0.x; {nm[1]} = L0.y; {nm[2]} = L1.x; {nm[3]} = L1.y;")
             w.ind -= 1
             w("}")
+        w.ind -= 1
+        w("}")
+        for ci, nm in names.items():
+            sl = slots[thr[ci][0]]
+            for q in range(4):
+                P.coup.add(w, nm[q], sl + q, [])
+        for kk, nm in regn.items():
+            sl = slots[reg_w[kk]]
+            for q in range(4):
+                P.coup.add(w, nm[q], sl + q, [])
+        P.coup.flush(w)
         w.ind -= 1
         w("}")
 

@@ -215,6 +215,29 @@ def build_plan(circuit, batch: int, objective: "Objective" = None, timer=None, r
     return Plan(machine_id(), n, batch, objective, tuple(assignments), tuple(measurements), tile_bits)
 
 
+def choose_tile_bits(circuit, batch: int, objective: "Objective" = None, candidates=TILE_BITS_CANDIDATES,
+                     reps: int = 3, warmup: int = 2, device=None, timer=None):
+    """Tile exponent M by measurement only (step 1 of build_plan without the per-layer
+    variants): every candidate <= n is timed on the whole program. Returns (M, {M: stats})."""
+    objective = objective or Objective.FORWARD_BACKWARD
+    n = int(circuit.n)
+    cands = sorted({min(n, m) for m in candidates})
+    stats = {m: time_program(circuit, batch, objective, M=m, reps=reps, warmup=warmup, timer=timer,
+                             device=device) for m in cands}
+    best = min(cands, key=lambda m: (stats[m].mean_seconds, -m))
+    return best, stats
+
+
+def plan_for_tile_bits(circuit, batch: int, tile_bits: int, objective: "Objective" = None,
+                       stats: dict | None = None) -> "Plan":
+    """All-FUSED plan with the given tile exponent (the measured candidates recorded as
+    layer_index -1 measurements are not part of the reference format, so they are dropped)."""
+    objective = objective or Objective.FORWARD_BACKWARD
+    n = int(circuit.n)
+    return Plan(machine_id(), n, batch, objective, tuple(KernelKind.FUSED for _ in circuit.layers), (),
+                int(tile_bits))
+
+
 def machine_id() -> str:
     try:
         import ctypes

@@ -207,6 +207,20 @@ def test_build_plan_real_timing_and_replay():
     assert_grads_close(a.grads, b.grads)
 
 
+def test_choose_tile_bits_and_plan_replay():
+    """Measured tile exponent (bench default) replayed through the public gradient()."""
+    from paper_2506_04891_b200 import planner as P
+
+    wl = make_workload(2, n=14, batch=8)
+    M, st = P.choose_tile_bits(wl.circuit, 8, reps=2, warmup=1)
+    assert M in st and set(st) == {10, 11, 12, 13}
+    plan = P.plan_for_tile_bits(wl.circuit, 8, M)
+    a = gradient(wl.circuit, wl.theta, wl.x, batch=8, weights=wl.weights, plan=plan)
+    ref = orc.gradient(wl.circuit, wl.theta, wl.x, batch=8, weights=wl.weights)
+    np.testing.assert_allclose(a.zq, ref["zq"], atol=Z_TOL)
+    assert_grads_close(a.grads, ref["grads"])
+
+
 @pytest.mark.parametrize("cfg,n,b", [(1, 8, 5), (2, 14, 3), (3, 13, 2), (4, 13, 2), (5, 14, 2)])
 def test_product_state_prefix_engine(cfg, n, b):
     """Synthesized product-state prefix + Lambda couplings vs the plain program vs oracle."""

@@ -106,3 +106,12 @@ def test_timing_stats_validation():
         P.TimingStats(1.0, 0.0, 0, 0)
     with pytest.raises(ValueError):
         P.TimingStats(-1.0, 0.0, 1, 0)
+
+
+def test_plan_for_tile_bits_roundtrip_and_validation():
+    circ = build_config_circuit(2)
+    plan = P.plan_for_tile_bits(circ, 16, 11)
+    assert plan.tile_bits == 11 and all(k is P.KernelKind.FUSED for k in plan.assignments)
+    assert plan_kernels(circ, plan) == list(plan.assignments)
+    assert P.plan_roundtrip(plan) == plan
+    assert P.tiling_of(plan, circ) == (11, None)
