@@ -938,27 +938,51 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
                      f"(__popcll(tbase & {nmask}ull) & 1)" if nmask else "0", str(c)]
             w(f"const float sg{q} = ((({' ^ '.join(terms)}) & 1) ? -1.f : 1.f);")
 
+    def emit_wht(init, dst):
+        """dst[m] = sum_i (-1)^popc(i & m) x[i] over the 2^R register indices, x[i] = init(i)."""
+        w(f"float {dst}[{P.NR}];")
+        for i in range(P.NR):
+            w(f"{dst}[{i}] = {init(i)};")
+        for b in range(P.R):
+            for i in range(P.NR):
+                if (i >> b) & 1:
+                    continue
+                jj = i | (1 << b)
+                w(f"{{ const float a_ = {dst}[{i}], b_ = {dst}[{jj}]; {dst}[{i}] = a_ + b_; {dst}[{jj}] = a_ - b_; }}")
+
     def emit_zpart_obs(k):
         w("{")
         w.ind += 1
         emit_obs_signs(k)
-        w(f"float pz[{P.n + 1}];")
-        w("float S_ = 0.f;")
-        for i in range(P.NR):
-            w(f"const float pr{i} = v[0][{i}].x * v[0][{i}].x + v[0][{i}].y * v[0][{i}].y;")
-        w(f"S_ = {' + '.join(f'pr{i}' for i in range(P.NR))};")
-        for q in range(P.n):
-            rmask = obs_parts(k, q)[0]
-            terms = " ".join(f"{'-' if bin(i & rmask).count('1') & 1 else '+'} pr{i}" for i in range(P.NR))
-            w(f"pz[{q}] = sg{q} * (0.f {terms});")
-        w(f"pz[{P.n}] = S_;")
-        w(f"warp_sum<NT, {P.n + 1}>(pz);")
-        w.block("if ((tid & 31) == 0)")
+        emit_wht(lambda i: f"v[0][{i}].x * v[0][{i}].x + v[0][{i}].y * v[0][{i}].y", "hz_")
+        vals = [f"sg{q} * hz_[{obs_parts(k, q)[0]}]" for q in range(P.n)] + ["hz_[0]"]
+        offs = [P.n - 1 - q for q in range(P.n)] + [P.n]
         w("float* zw = s_zw + warp * 32;")
-        for q in range(P.n):
-            w(f"zw[{P.n - 1 - q}] += pz[{q}];")
-        w(f"zw[{P.n}] += pz[{P.n}];")
-        w.end()
+        npad = (-len(vals)) % 8
+        if P.NT >= 32 and len(vals) + npad <= 32:
+            # reduce-scatter 8 values per call; zero padding goes to the unused tail slots
+            pad_offs = list(range(P.n + 1, P.n + 1 + npad))
+            vals += ["0.f"] * npad
+            offs += pad_offs
+            for c0 in range(0, len(vals), 8):
+                ov = offs[c0:c0 + 8]
+                exprs = []
+                for h in (0, 4):
+                    o = ov[h:h + 4]
+                    d = o[1] - o[0]
+                    if all(o[t] == o[0] + d * t for t in range(4)):
+                        exprs.append(f"{o[0]} + {d} * lj_")
+                    else:
+                        exprs.append(f"(lj_ & 2 ? (lj_ & 1 ? {o[3]} : {o[2]}) : (lj_ & 1 ? {o[1]} : {o[0]}))")
+                w(f"{{ float a8_[8] = {{{', '.join(vals[c0:c0 + 8])}}}; "
+                  f"warp_accumulate8p<NT>(a8_, zw + (hi16_ ? {exprs[1]} : {exprs[0]})); }}")
+        else:
+            w(f"float pz[{len(vals)}] = {{{', '.join(vals)}}};")
+            w(f"warp_sum<NT, {len(vals)}>(pz);")
+            w.block("if ((tid & 31) == 0)")
+            for e, o in enumerate(offs):
+                w(f"zw[{o}] += pz[{e}];")
+            w.end()
         w.ind -= 1
         w("}")
 
@@ -966,11 +990,14 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
         w("{")
         w.ind += 1
         emit_obs_signs(k)
+        # o_i = sum_q ws_q (-1)^popc(i & rmask_q): collect ws by register mask, then one WHT
+        byr = {}
         for q in range(P.n):
-            w(f"const float ws{q} = sg{q} * (A.wts ? (float)A.wts[{q}] : 1.f);")
+            byr.setdefault(obs_parts(k, q)[0], []).append(q)
+        wsum = {m: " + ".join(f"sg{q} * (A.wts ? (float)A.wts[{q}] : 1.f)" for q in qs) for m, qs in byr.items()}
+        emit_wht(lambda i: wsum.get(i, "0.f"), "ow_")
         for i in range(P.NR):
-            terms = " ".join(f"{'-' if bin(i & obs_parts(k, q)[0]).count('1') & 1 else '+'} ws{q}" for q in range(P.n))
-            w(f"{{ const float o = 0.f {terms}; v[1][{i}] = make_float2(o * v[0][{i}].x, o * v[0][{i}].y); }}")
+            w(f"v[1][{i}] = make_float2(ow_[{i}] * v[0][{i}].x, ow_[{i}] * v[0][{i}].y);")
         w.ind -= 1
         w("}")
 
