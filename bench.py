@@ -250,6 +250,18 @@ def _pass_vectors(prog, mode, pidx, adjoint="recompute"):
     return 2 + writes
 
 
+MODE_NAMES = {0: "forward", 1: "turnaround", 2: "adjoint"}
+
+
+def _kernel_label(eng, mode, pidx):
+    """Kernel family of one pass launch: the specialised kernels are lsq_jit_p<pass>_m<mode>
+    (NVRTC, one per pass and mode), the generic ones lsq_pass_kernel<M, NV>."""
+    M = eng.program.passes[pidx].M
+    if eng.variant == "jit":
+        return "lsq_jit_p*_m%d (%s, M=%d)" % (mode, MODE_NAMES[mode], M)
+    return "lsq_pass_kernel<M=%d,NV=%d>" % (M, 1 if mode == 0 else 2)
+
+
 def run_ours(args, world, rank, local):
     import torch
 
@@ -339,7 +351,7 @@ def run_ours(args, world, rank, local):
         for kind, t, rows_launch in eng.native.profile:
             mode, pidx = divmod(kind, 1000)
             vec = _pass_vectors(eng.program, mode, pidx, eng.last_adjoint)
-            key = "lsq_pass_kernel<M=%d,NV=%d>" % (eng.program.passes[pidx].M, 1 if mode == 0 else 2)
+            key = _kernel_label(eng, mode, pidx)
             d = per_kernel.setdefault(key, {"bytes": 0.0, "ms": 0.0, "launches": 0})
             d["bytes"] += vec * rows_launch * (8 << n)
             d["ms"] += t
@@ -354,7 +366,7 @@ def run_ours(args, world, rank, local):
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get(dom[0])
+            traffic = json.load(open(prof)).get(f"{CONFIG_NAMES[cfg]}|{dom[0]}")
         except Exception:
             traffic = None
     roofline = {

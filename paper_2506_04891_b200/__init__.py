@@ -49,6 +49,10 @@ def __getattr__(name):
         "save_plan": ("planner", "save_plan"),
         "load_plan": ("planner", "load_plan"),
         "plan_roundtrip": ("planner", "plan_roundtrip"),
+        "choose_tile_bits": ("planner", "choose_tile_bits"),
+        "plan_for_tile_bits": ("planner", "plan_for_tile_bits"),
+        "expectation": ("autograd", "expectation"),
+        "QuantumLayer": ("autograd", "QuantumLayer"),
     }
     if name in lazy:
         import importlib

@@ -233,3 +233,44 @@ def test_product_state_prefix_engine(cfg, n, b):
         np.testing.assert_allclose(r["zq"].cpu().numpy(), ref["zq"], atol=Z_TOL)
         assert_grads_close(r["grads"].cpu().numpy(), ref["grads"])
         assert_grads_close(r["encoding_grads"].cpu().numpy(), ref["encoding_grads"], "encoding")
+
+
+def test_autograd_expectation_matches_oracle():
+    """torch.autograd integration: d(sum_b c_b value_b)/d(theta, x, w) vs the oracle's per-row
+    gradients contracted with c."""
+    import torch
+
+    from paper_2506_04891_b200.autograd import expectation
+
+    wl = make_workload(2, n=10, batch=6)
+    ref = orc.gradient(wl.circuit, wl.theta, wl.x, batch=6, weights=wl.weights, need_encoding=True)
+    th = torch.tensor(wl.theta, dtype=torch.float64, device="cuda", requires_grad=True)
+    x = torch.tensor(wl.x, dtype=torch.float64, device="cuda", requires_grad=True)
+    w = torch.tensor(wl.weights, dtype=torch.float64, device="cuda", requires_grad=True)
+    c = torch.linspace(-1.0, 2.0, 6, dtype=torch.float64, device="cuda")
+    val = expectation(wl.circuit, th, x, w)
+    np.testing.assert_allclose(val.detach().cpu().numpy(), ref["value"], atol=Z_TOL * wl.n)
+    (val * c).sum().backward()
+    cn = c.cpu().numpy()
+    assert_grads_close(th.grad.cpu().numpy()[None], (cn @ ref["grads"])[None])
+    assert_grads_close(x.grad.cpu().numpy(), cn[:, None] * ref["encoding_grads"])
+    np.testing.assert_allclose(w.grad.cpu().numpy(), cn @ ref["zq"], atol=1e-5)
+
+
+def test_quantum_layer_training_loop_decreases_loss():
+    import torch
+
+    from paper_2506_04891_b200.autograd import QuantumLayer
+
+    wl = make_workload(1, batch=16)
+    layer = QuantumLayer(wl.circuit, seed=3)
+    opt = torch.optim.Adam(layer.parameters(), lr=0.1)
+    x = torch.tensor(wl.x, dtype=torch.float64, device="cuda")
+    losses = []
+    for _ in range(8):
+        opt.zero_grad()
+        loss = layer(x).mean()
+        loss.backward()
+        opt.step()
+        losses.append(float(loss))
+    assert losses[-1] < losses[0] - 0.1, losses
