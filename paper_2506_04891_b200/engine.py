@@ -260,9 +260,10 @@ class Engine:
         return "ckpt" if self.micro_batch(batch, L) >= min(batch, 16) else "recompute"
 
     def fwd_bwd(self, trainable=None, encoding=None, batch=1, weights=None, rows=True,
-                encoding_grads=True, micro_batch=None, buffers=None, checkpoint=None):
+                encoding_grads=True, micro_batch=None, buffers=None, checkpoint=None, out=None):
         """Forward from |0..0> plus adjoint backward. Returns a dict of CUDA tensors:
-        value (B,), zq (B,n), grads (B,T) if rows, grad_sum (T,), encoding_grads (B,E)."""
+        value (B,), zq (B,n), grads (B,T) if rows, grad_sum (T,), encoding_grads (B,E).
+        `out`: optional preallocated float64 tensors with those keys (written in place)."""
         th, x, w = self._params(trainable, encoding, weights, batch)
         mode = self.adjoint_mode(batch, checkpoint)
         L = len(self.program.passes)
@@ -271,12 +272,21 @@ class Engine:
         self.last_micro_batch, self.last_adjoint = mb, mode
         dev = self.device
         f64 = dict(dtype=torch.float64, device=dev)
-        value = torch.empty((batch,), **f64)
-        zq = torch.empty((batch, self.n), **f64)
-        grows = torch.empty((batch, self.T), **f64) if (rows and self.T) else None
-        erows = torch.empty((batch, self.E), **f64) if (encoding_grads and self.E) else None
+        o = out or {}
+        value = o["value"] if "value" in o else torch.empty((batch,), **f64)
+        zq = o["zq"] if "zq" in o else torch.empty((batch, self.n), **f64)
+        grows = None
+        if rows and self.T:
+            grows = o["grads"] if o.get("grads") is not None else torch.empty((batch, self.T), **f64)
+        erows = None
+        if encoding_grads and self.E:
+            erows = (o["encoding_grads"] if o.get("encoding_grads") is not None
+                     else torch.empty((batch, self.E), **f64))
         nchunk = (batch + mb - 1) // mb
-        gparts = torch.zeros((nchunk, max(self.T, 1)), **f64)
+        if nchunk == 1 and o.get("grad_sum") is not None and self.T:
+            gparts = o["grad_sum"].view(1, self.T)
+        else:
+            gparts = torch.zeros((nchunk, max(self.T, 1)), **f64)
         def fits(bufs):
             return (bufs is not None and bufs[0].shape[0] >= mb
                     and (mode == "recompute" or (bufs[2] is not None and bufs[2].shape[1] >= mb
@@ -320,6 +330,9 @@ class Engine:
             if self.native.profiling:
                 self.native.profile += [(k, ms, b) for k, ms in self.native.pass_times()]
         gsum = gparts.sum(dim=0)[: self.T] if nchunk > 1 else gparts[0, : self.T]
+        if o.get("grad_sum") is not None and gsum.data_ptr() != o["grad_sum"].data_ptr():
+            o["grad_sum"].copy_(gsum)
+            gsum = o["grad_sum"]
         return {"value": value, "zq": zq, "grads": grows, "grad_sum": gsum, "encoding_grads": erows,
                 "buffers": (psi, lam, ck), "adjoint": mode}
 
@@ -371,9 +384,31 @@ class GradStep:
         self.batch = int(batch)
         dev = eng.device
         f64 = dict(dtype=torch.float64, device=dev)
-        self.theta = torch.zeros((max(eng.T, 1),), **f64)
-        self.x = torch.zeros((self.batch, max(eng.E, 1)), **f64)
-        self.w = torch.ones((eng.n,), **f64)
+        B, T, E, n = self.batch, eng.T, eng.E, eng.n
+        # one flat input buffer (theta | x | w) and one flat output buffer (value | zq | grads |
+        # grad_sum | encoding_grads): host I/O is one pinned copy each way (run_host)
+        nT, nE = max(T, 1), max(E, 1)
+        self.d_in = torch.zeros((nT + B * nE + n,), **f64)
+        self.theta = self.d_in[:nT]
+        self.x = self.d_in[nT : nT + B * nE].view(B, nE)
+        self.w = self.d_in[nT + B * nE :]
+        self.w.fill_(1.0)
+        sizes = [("value", (B,)), ("zq", (B, n))]
+        if rows and T:
+            sizes.append(("grads", (B, T)))
+        if T:
+            sizes.append(("grad_sum", (T,)))
+        if encoding_grads and E:
+            sizes.append(("encoding_grads", (B, E)))
+        tot = sum(int(np.prod(sh)) for _, sh in sizes)
+        self.d_out = torch.zeros((tot,), **f64)
+        self.out_views, off = {}, 0
+        for k, sh in sizes:
+            m = int(np.prod(sh))
+            self.out_views[k] = (off, sh)
+            off += m
+        self.outbuf = {k: self.d_out[o : o + int(np.prod(sh))].view(sh) for k, (o, sh) in self.out_views.items()}
+        self.h_in = self.h_out = None
         self.kw = dict(batch=self.batch, rows=rows, encoding_grads=encoding_grads, checkpoint=checkpoint)
         if graph is None:
             graph = os.environ.get("LSQ_GRAPHS", "1") != "0"
@@ -390,7 +425,7 @@ class GradStep:
         e = self.eng
         th = self.theta[: e.T] if e.T else None
         x = self.x[:, : e.E] if e.E else None
-        return e.fwd_bwd(th, x, weights=self.w, **self.kw)
+        return e.fwd_bwd(th, x, weights=self.w, out=self.outbuf, **self.kw)
 
     def set_inputs(self, theta=None, x=None, w=None):
         e = self.eng
@@ -408,6 +443,34 @@ class GradStep:
         else:
             self.out = self._call()
         return self.out
+
+    def run_host(self, theta=None, x=None, w=None) -> dict:
+        """Host numpy in, host numpy out: the inputs are packed into a pinned staging buffer and
+        sent with ONE host-to-device copy, the graph is replayed, and every output comes back
+        with ONE device-to-host copy (then copied out of the reused pinned buffer)."""
+        e = self.eng
+        if self.h_in is None:
+            self.h_in = torch.empty(self.d_in.shape, dtype=torch.float64, pin_memory=True)
+            self.h_out = torch.empty(self.d_out.shape, dtype=torch.float64, pin_memory=True)
+            self.h_in.copy_(self.d_in)
+        hi = self.h_in.numpy()
+        nT, nE = self.theta.shape[0], self.x.shape[1]
+        if theta is not None and e.T:
+            hi[: e.T] = np.asarray(theta, dtype=np.float64).reshape(-1)
+        if x is not None and e.E:
+            hi[nT : nT + self.batch * nE].reshape(self.batch, nE)[:, : e.E] = np.asarray(x, dtype=np.float64)
+        if w is not None:
+            hi[nT + self.batch * nE :] = np.asarray(w, dtype=np.float64).reshape(-1)
+        stream = torch.cuda.current_stream(e.device)
+        self.d_in.copy_(self.h_in, non_blocking=True)
+        if self.graph is not None:
+            self.graph.replay()
+        else:
+            self.out = self._call()
+        self.h_out.copy_(self.d_out, non_blocking=True)
+        stream.synchronize()
+        ho = self.h_out.numpy()
+        return {k: ho[o : o + int(np.prod(sh))].reshape(sh).copy() for k, (o, sh) in self.out_views.items()}
 
 
 _CACHE: "OrderedDict" = None

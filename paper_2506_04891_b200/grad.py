@@ -54,8 +54,16 @@ def gradient(circuit, trainable=None, encoding=None, batch: int = 1, plan=None, 
     if step is None:
         steps.clear()  # keep one step's static buffers alive per engine
         step = steps[key] = eng.make_step(batch)
-    r = step.run(trainable, encoding, np.ones(circuit.n) if weights is None else weights)
     T, E = eng.T, eng.E
+    host = not any(type(a).__module__.startswith("torch") for a in (trainable, encoding, weights))
+    if host:
+        # host arrays in and out: one pinned copy each way around the graph replay
+        r = step.run_host(trainable, encoding, np.ones(circuit.n) if weights is None else weights)
+        z = lambda k, sh: r[k] if k in r else np.zeros(sh)  # noqa: E731
+        return GradResult(value=z("value", (batch,)), grads=z("grads", (batch, T)),
+                          encoding_grads=z("encoding_grads", (batch, E)), zq=z("zq", (batch, circuit.n)),
+                          grad_sum=z("grad_sum", (T,)))
+    r = step.run(trainable, encoding, np.ones(circuit.n) if weights is None else weights)
     return GradResult(
         value=_np(r["value"], (batch,)),
         grads=_np(r["grads"], (batch, T)),
