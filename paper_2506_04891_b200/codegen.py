@@ -257,6 +257,23 @@ _COMP_TERMS = {
 }
 
 
+def _tree_sum(terms):
+    """Balanced addition tree (fp adds are not reassociated by the compiler: a left-leaning
+    chain of 15 adds is 15 dependent latencies, the tree 4)."""
+    terms = list(terms)
+    if not terms:
+        return "0.f"
+    while len(terms) > 1:
+        nxt = [f"({terms[q]} + {terms[q + 1]})" for q in range(0, len(terms) - 1, 2)]
+        if len(terms) % 2:
+            nxt.append(terms[-1])
+        terms = nxt
+    return terms[0]
+
+
+COUPLING_CHAINS = 2  # independent partial accumulators per coupling component (ILP)
+
+
 def _emit_u1_coupling(w, P, k, slot, comps):
     lay = coupling_layout(comps)
     if not lay:
@@ -265,14 +282,18 @@ def _emit_u1_coupling(w, P, k, slot, comps):
     w("{")
     w.ind += 1
     pairs = [(i, i | (1 << k)) for i in range(1 << P.R) if not (i >> k) & 1]
+    nch = max(1, min(COUPLING_CHAINS, len(pairs)))
     for ci, (nm, _pos) in enumerate(lay):
-        acc = None
-        for (i, j) in pairs:
+        accs = [None] * nch
+        for pi, (i, j) in enumerate(pairs):
             idx = {"i": i, "j": j}
+            c = pi % nch
             for fn, li, pi_ in _COMP_TERMS[nm]:
                 a, b = f"v[1][{idx[li]}]", f"v[0][{idx[pi_]}]"
-                acc = f"vm{fn}({a}, {b})" if acc is None else f"vf{fn}({a}, {b}, {acc})"
-        w(f"{{ const float2 t_ = {acc}; {names[ci]} = t_.x + t_.y; }}")
+                accs[c] = f"vm{fn}({a}, {b})" if accs[c] is None else f"vf{fn}({a}, {b}, {accs[c]})"
+        for c in range(nch):
+            w(f"const float2 t{ci}_{c} = {accs[c]};")
+        w(f"{names[ci]} = {_tree_sum([f't{ci}_{c}.x' for c in range(nch)] + [f't{ci}_{c}.y' for c in range(nch)])};")
     w.ind -= 1
     w("}")
     used = {pos for _, pos in lay}
@@ -460,7 +481,7 @@ def _emit_drun(w, P, op, ph_idx, mode_bwd, nv):
                 terms.setdefault(e, []).append(i)
             w(" ".join(f"{nm[k]} = -0.f;" for k in range(1 << ar)))
             for e, idxs in terms.items():
-                sy = " + ".join(f"c{i}" for i in idxs)
+                sy = _tree_sum([f"c{i}" for i in idxs])
                 if ar == 1:
                     ix = str(e) if e is not None else ea
                 else:

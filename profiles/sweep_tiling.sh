@@ -13,7 +13,7 @@ try:
     d = json.loads(open(f).read().strip().splitlines()[-1])
     pk = d["roofline"]["per_kernel"]
     print(f"coal={__import__('os').environ.get('LSQ_COAL','4')} M={M} R={R} evals/s={d['value']:.0f} ms/step={d['ms_per_step']:.3f} passes={d['config']['passes']} " +
-          " ".join(f"{k.split('<')[1][:-1]}:{v['GBps']}GB/s,{v['ms_per_step']:.2f}ms" for k, v in pk.items()))
+          " ".join(f"{k.split(' ')[0].split('_')[-1]}:{v['GBps']}GB/s,{v['ms_per_step']:.2f}ms" for k, v in pk.items()))
 except Exception as e:
     print(f"M={M} R={R} failed: {e}"); print(open(f).read()[-800:])
 PY
