@@ -705,6 +705,13 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
     w(f"const size_t rowbase = (size_t)row << {P.n};")
     w("const int t0 = cslot * A.tiles_per_cta, t_end = t0 + A.tiles_per_cta;")
     last = nph - 1
+    # adjoint and turnaround kernels read their tile from the prefetch stage, where any layout
+    # is free: an empty last phase (kept only so forward stores are coalesced) is skipped,
+    # saving one transpose per vector
+    top = last
+    if (mode != MODE_FWD and prefetch and nph > 1 and len(P.enc["ops"][last]) == 0
+            and os.environ.get("LSQ_SKIP_EMPTY", "1") != "0"):
+        top = last - 1
     # ---- next-tile prefetch: cp.async 16-byte chunks into the stage (natural local order).
     # chunk c holds local amplitudes (2c, 2c+1); c = (tid low bits) + j * 2^tid_bits.
     nchunk = 1 << (P.M - 1)
@@ -933,10 +940,10 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
         w.ind -= 1
         w("}")
 
-    def emit_fwd_phases():
-        for k in range(nph):
+    def emit_fwd_phases(end):
+        for k in range(end + 1):
             _emit_ops(w, P, k, False, nv)
-            if k < last:
+            if k < end:
                 _emit_exchange(w, P, k, k + 1, nv)
 
     obs = getattr(prog, "obs", None) if mode == MODE_TURN else None
@@ -1081,7 +1088,7 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
         w("}")
 
     def emit_bwd_phases():
-        for k in range(last, -1, -1):
+        for k in range(top, -1, -1):
             _emit_ops(w, P, k, True, nv)
             if k > 0:
                 _emit_exchange(w, P, k, k - 1, nv)
@@ -1104,13 +1111,13 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
         w.block("if (!do_load)")
         emit_synth(0)
         w.end()
-        emit_fwd_phases()
+        emit_fwd_phases(last)
         w.block("if (flags & PF_ZPART)")
         emit_zpart(last)
         w.end()
         emit_store(last, "psi")
     elif mode == MODE_BWD:
-        emit_load(last)
+        emit_load(top)
         emit_bwd_phases()
         if use_prefix:
             emit_prefix_lambda(0)
@@ -1119,7 +1126,7 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
     else:
         # turnaround: forward phases (unless NOFWD), <Z>, lambda = O psi, adjoint phases
         w.block("if (nofwd)")
-        emit_load(last)
+        emit_load(top)
         w.end()
         w.block("else")
         w.block("if (do_load)")
@@ -1128,10 +1135,10 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
         w.block("else")
         emit_synth(0)
         w.end()
-        emit_fwd_phases()
+        emit_fwd_phases(top)
         w.end()
-        emit_zpart(last)
-        emit_lambda_init(last)
+        emit_zpart(top)
+        emit_lambda_init(top)
         emit_bwd_phases()
         if use_prefix and len(prog.passes) == 1:
             emit_prefix_lambda(0)
