@@ -451,12 +451,120 @@ class _Coup:
             w(f"{{ {init} warp_sum<NT, 8>(a8_); if ((tid & 31) == 0) {{ {' '.join(adds)} }} }}")
 
 
+_DIAG_COMP_CACHE: dict = {}
+
+
+def diag_components(grp, samples: int = 3):
+    """Nonzero Walsh components of a diagonal group's phase derivatives.
+
+    G = diag(e^{i alpha_e}) over the 2^ar classes e (first wire = MSB). Every free parameter
+    p has dalpha_p/dtheta = sum_c a_{p,c} w_c(e) with w_c(e) = (-1)^popc(c & e). The gradient
+    is -2 sum_e alpha'_{p,e} S_e, S_e = sum over class e of Im(conj(lam) psi): it only needs
+    the component sums V_c = sum_e w_c(e) S_e for the c with a_{p,c} != 0. The constant
+    component c = 0 multiplies Im<lam|psi> over the row, which is 0 (lam and psi evolve under
+    the same unitaries from lam = O psi with O Hermitian), so it is never accumulated."""
+    from .gates import gate_matrix, gate_matrix_derivative
+
+    key = tuple((g.kind, tuple(g.src), tuple(g.fixed), rev) for g, rev in grp.gates)
+    if key in _DIAG_COMP_CACHE:
+        return _DIAG_COMP_CACHE[key]
+    d = 1 << grp.arity
+    rng = np.random.default_rng(4321)
+    comps = set()
+    for _ in range(samples):
+        mats, ders = [], []
+        for g, rev in grp.gates:
+            k = GATE_TRAITS[g.kind].param_count
+            prm = [g.fixed[j] if g.src[j] == S.FIXED_SRC else float(rng.uniform(-3.0, 3.0)) for j in range(k)]
+            G = np.diag(np.diag(gate_matrix(g.kind, prm) if k else gate_matrix(g.kind)))
+            dl = [np.diag(np.diag(gate_matrix_derivative(g.kind, prm, j))) for j in range(k) if g.src[j] != S.FIXED_SRC]
+            if rev and d == 4:  # gate given on (b, a): swap the two wires of the class index
+                perm = [0, 2, 1, 3]
+                G = G[np.ix_(perm, perm)]
+                dl = [D[np.ix_(perm, perm)] for D in dl]
+            mats.append(G)
+            ders.append(dl)
+        U = np.eye(d, dtype=complex)
+        for G in mats:
+            U = G @ U
+        for j, dl in enumerate(ders):
+            for dG in dl:
+                full = np.eye(d, dtype=complex)
+                for jj, G in enumerate(mats):
+                    full = (dG if jj == j else G) @ full
+                ap = np.imag(np.diag(full) / np.diag(U))  # alpha'_e
+                for c in range(1, d):
+                    wc = np.array([(-1) ** bin(c & e).count("1") for e in range(d)])
+                    if abs(ap @ wc) / d > 1e-9:
+                        comps.add(c)
+    out = tuple(sorted(comps))
+    _DIAG_COMP_CACHE[key] = out
+    return out
+
+
+def _emit_drun_walsh(w, P, subs, tp):
+    """Diagonal couplings as Walsh component sums (see diag_components): per distinct
+    register mask m one packed chain T_m = sum_i (-1)^popc(i & m) lam_i .* (psi_i.y, -psi_i.x),
+    V = T.x + T.y; thread and tile bits of a component only flip its sign. Component c of a
+    sub goes to slot float 2c - 1; the CTA epilogue (P.walsh) expands the components into the
+    per-class values S'_e the contraction kernel reads."""
+    R = P.R
+    plan = []  # (sub index, slot, ar, comp, regmask, sign expressions)
+    for si, s in enumerate(subs):
+        slot = int(s[4])
+        if slot < 0:
+            continue
+        grp = P.prog.groups[int(s[2])]
+        ar = int(s[5])
+        srcs = [_src_expr(s[0], P, tp)] + ([_src_expr(s[1], P, tp)] if ar == 2 else [])
+        comps = diag_components(grp)
+        for c in comps:
+            regmask, signs = 0, []
+            for q, (kind, e) in enumerate(srcs):
+                bit = (c >> (ar - 1 - q)) & 1  # class index e = 2 a + b: wire a is the MSB
+                if not bit:
+                    continue
+                if kind == "reg":
+                    regmask ^= 1 << e
+                else:
+                    signs.append(e)
+            plan.append((si, slot, ar, c, regmask, signs))
+        P.walsh.append((slot, ar, comps))
+    masks = sorted({pl[4] for pl in plan})
+    names = [P.coup.new(w) for _ in plan]
+    w("{")
+    w.ind += 1
+    nch = COUPLING_CHAINS
+    for m in masks:
+        accs = [None] * nch
+        for i in range(P.NR):
+            fn = "_j" if bin(i & m).count("1") & 1 else "_mj"
+            c = i % nch
+            accs[c] = f"vm{fn}(v[1][{i}], v[0][{i}])" if accs[c] is None else f"vf{fn}(v[1][{i}], v[0][{i}], {accs[c]})"
+        for c in range(nch):
+            w(f"const float2 wt{m}_{c} = {accs[c]};")
+        w(f"const float wv{m} = {_tree_sum([f'wt{m}_{c}.x' for c in range(nch)] + [f'wt{m}_{c}.y' for c in range(nch)])};")
+    for (si, slot, ar, c, regmask, signs), nm in zip(plan, names):
+        if signs:
+            par = " ^ ".join(f"(int)({e})" for e in signs)
+            w(f"{nm} = (({par}) & 1) ? -wv{regmask} : wv{regmask};")
+        else:
+            w(f"{nm} = wv{regmask};")
+    w.ind -= 1
+    w("}")
+    for (si, slot, ar, c, regmask, signs), nm in zip(plan, names):
+        used = {slot + 2 * cc - 1 for cc in diag_components(P.prog.groups[int(subs[si][2])])}
+        free = [slot + q for q in range(2 << ar) if slot + q not in used]
+        P.coup.add(w, nm, slot + 2 * c - 1, free)
+
 def _emit_drun(w, P, op, ph_idx, mode_bwd, nv):
     subs = P.enc["subs"][op[6] : op[6] + op[7]]
     tp = f"tp{ph_idx}"
     R = P.R
     # couplings (backward, before un-applying: conj(l) p is phase invariant)
-    if mode_bwd and any(int(s[4]) >= 0 for s in subs):
+    if mode_bwd and any(int(s[4]) >= 0 for s in subs) and P.walsh_diag:
+        _emit_drun_walsh(w, P, subs, tp)
+    elif mode_bwd and any(int(s[4]) >= 0 for s in subs):
         names = {si: [P.coup.new(w) for _ in range(1 << int(s[5]))] for si, s in enumerate(subs) if int(s[4]) >= 0}
         w("{")
         w.ind += 1
@@ -636,6 +744,8 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
     P = _Pass(prog, pi)
     P.coup = _Coup(P)
     P.drop_phase = bool(getattr(prog, "drop_phase", False))
+    P.walsh_diag = os.environ.get("LSQ_WALSH_DIAG", "1") != "0"
+    P.walsh = []  # (slot, arity, components) of diagonal couplings kept as Walsh sums
     P.slotf = prog.enc[pi]["slotf"]
     nv = 1 if mode == MODE_FWD else 2
     prefetch = stage_vectors(prog, pi, mode) > 0
@@ -1151,6 +1261,19 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
         w.block("if (A.part)")
         w(f"double* dst = A.part + (size_t)blockIdx.x * {slotf};")
         w(f"for (int f = tid; f < {slotf}; f += NT) {{ double s = 0.0; for (int ww = 0; ww < NW; ++ww) s += (double)s_acc[ww * {slotf + 8} + f]; dst[f] = s; }}")
+        if P.walsh:
+            # Walsh component sums -> per-class values S'_e = 2^-ar sum_c V_c (-1)^popc(c & e)
+            # (the constant component is dropped: it multiplies Im<lam|psi> = 0)
+            w("__syncthreads();")
+            for idx, (slot, ar, comps) in enumerate(P.walsh):
+                d = 1 << ar
+                w.block(f"if (tid == {idx % P.NT})")
+                for c in comps:
+                    w(f"double V{c} = 0.0; for (int ww = 0; ww < NW; ++ww) V{c} += (double)s_acc[ww * {slotf + 8} + {slot + 2 * c - 1}];")
+                for e in range(d):
+                    terms = " ".join(f"{'-' if bin(c & e).count('1') & 1 else '+'} V{c}" for c in comps)
+                    w(f"dst[{slot + 2 * e}] = 0.0; dst[{slot + 2 * e + 1}] = ({terms}) * {1.0 / d!r};")
+                w.end()
         w.end()
     w.block(f"if ((mode == PMODE_TURN || (flags & PF_ZPART)) && A.zpart)")
     w(f"double* dst = A.zpart + (size_t)blockIdx.x * {P.n + 1};")
