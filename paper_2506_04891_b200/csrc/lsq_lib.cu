@@ -254,6 +254,7 @@ struct JitKernel {
   const void* fn = nullptr;  // cudaKernel_t usable as a function handle
   int NT = 0;
   size_t smem_set = 0;
+  int occ = 0;  // resident CTAs per SM at smem_set (cudaOccupancyMaxActiveBlocksPerMultiprocessor)
 };
 
 struct lsq_program {
@@ -306,9 +307,31 @@ struct Geometry {
   int tpc, cpr;
 };
 
-Geometry geometry(const lsq_program* P, const PassInfo& pi, int batch) {
+// Tiles per CTA. With the resident capacity G = occ x SMs of the specialised kernel known,
+// tpc minimises waves x (tpc + 1/2): whole waves of equal CTAs (a partial last wave leaves
+// SMs idle) against the per-CTA prologue (table staging, first tile load, partial flush),
+// costed at half a tile. Without it: about 4 CTAs per SM of 64 tiles at most.
+Geometry geometry(const lsq_program* P, int pidx, int mode, int batch) {
+  const PassInfo& pi = P->passes[pidx];
   const int ntiles = 1 << (P->n - pi.M);
   const int64_t total = (int64_t)batch * ntiles;
+  int occ = 0;
+  if (!P->jit.empty() && mode >= 0 && P->jit[pidx * 3 + mode].fn) occ = P->jit[pidx * 3 + mode].occ;
+  if (occ > 0) {
+    const int64_t G = (int64_t)occ * P->sm_count;
+    int best_t = 1;
+    double best = 1e300;
+    for (int t = std::min(ntiles, 64); t >= 1; t >>= 1) {
+      const int64_t units = total / t;
+      const int64_t waves = (units + G - 1) / G;
+      const double cost = (double)waves * (t + 0.5);
+      if (cost < best * (1 - 1e-9)) {
+        best = cost;
+        best_t = t;
+      }
+    }
+    return Geometry{best_t, ntiles / best_t};
+  }
   const int64_t target = (int64_t)P->sm_count * 4;
   int tpc = total > target ? pow2floor(total / target) : 1;
   if (tpc > ntiles) tpc = ntiles;
@@ -337,11 +360,13 @@ WS carve(const lsq_program* P, int batch, void* base) {
     return o;
   };
   size_t maxpart = 0, maxz = 0;
-  for (const auto& pi : P->passes) {
-    Geometry g = geometry(P, pi, batch);
-    maxpart = std::max(maxpart, (size_t)batch * g.cpr * pi.slotf);
-    maxz = std::max(maxz, (size_t)batch * g.cpr * (P->n + 1));
-  }
+  for (int p = 0; p < (int)P->passes.size(); ++p)
+    for (int mode = -1; mode < 3; ++mode) {
+      const PassInfo& pi = P->passes[p];
+      Geometry g = geometry(P, p, mode, batch);
+      maxpart = std::max(maxpart, (size_t)batch * g.cpr * pi.slotf);
+      maxz = std::max(maxz, (size_t)batch * g.cpr * (P->n + 1));
+    }
   size_t o_g = take(sizeof(float) * 32 * (size_t)std::max(P->ngroups, 1));
   size_t o_r = take(sizeof(float) * 32 * (size_t)batch * std::max(P->nperrow, 1));
   size_t o_pt = take(sizeof(float) * 4 * (size_t)batch * (P->prefix ? P->n : 1));
@@ -377,7 +402,7 @@ int launch_pass(lsq_program* P, int pi_idx, int mode, int flags, int batch, cons
   if (!k.fn && !have_jit)
     return fail(LSQ_EPLAN, "no kernel for pass " + std::to_string(pi_idx) + " (M=" + std::to_string(pi.M) +
                                ", R=" + std::to_string(pi.R) + "): attach the specialised kernels");
-  Geometry g = geometry(P, pi, batch);
+  Geometry g = geometry(P, pi_idx, have_jit ? mode : -1, batch);
   PassArgs A{};
   A.prog = P->d_words;
   A.fvals = P->d_fvals;
@@ -712,6 +737,9 @@ int lsq_program_jit(lsq_program* P, int nk, const char* const* sources, const in
     const size_t sm = smem_bytes(P, pi, NV) + (size_t)sv * sizeof(float2) * ((size_t)1 << pi.M);
     CUDA_TRY(cudaFuncSetAttribute(jk.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     jk.smem_set = sm;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&jk.occ, jk.fn, jk.NT, sm));
+    const char* geo = getenv("LSQ_GEOM_OCC");  // "0": fixed 4-CTAs-per-SM heuristic (A/B runs)
+    if (geo && geo[0] == '0') jk.occ = 0;
   }
   return LSQ_OK;
 }
@@ -804,7 +832,7 @@ int lsq_forward(const lsq_program* Pc, int batch, const double* theta, const dou
     if (rc) return rc;
   }
   if (want_z) {
-    Geometry g = geometry(P, P->passes.back(), batch);
+    Geometry g = geometry(P, P->npasses - 1, MODE_FWD, batch);
     k_reduce_z<<<(batch + 127) / 128, 128, 0, st>>>(ws.zpart, g.cpr, P->n, w, zq, value, batch);
     P->launches++;
     CUDA_TRY(cudaGetLastError());
@@ -868,7 +896,7 @@ int lsq_fwd_bwd_ckpt(const lsq_program* Pc, int batch, const double* theta, cons
     const float2* in = L > 1 ? out_of(L - 2) : psi;
     int rc = launch_pass(P, L - 1, MODE_TURN, flags, batch, theta, x, x_stride, w, in, psi, lam, ws, st);
     if (rc) return rc;
-    Geometry g = geometry(P, P->passes[L - 1], batch);
+    Geometry g = geometry(P, L - 1, MODE_TURN, batch);
     k_reduce_z<<<(batch + 127) / 128, 128, 0, st>>>(ws.zpart, g.cpr, P->n, w, zq, value, batch);
     P->launches++;
     CUDA_TRY(cudaGetLastError());
@@ -921,7 +949,7 @@ int lsq_bwd_from_state(const lsq_program* Pc, int batch, const double* theta, co
     int rc = launch_pass(P, L - 1, MODE_TURN, flags, batch, theta, x, x_stride, w,
                          (const float2*)final_state, psi, lam, ws, st);
     if (rc) return rc;
-    Geometry g = geometry(P, P->passes[L - 1], batch);
+    Geometry g = geometry(P, L - 1, MODE_TURN, batch);
     k_reduce_z<<<(batch + 127) / 128, 128, 0, st>>>(ws.zpart, g.cpr, P->n, w, zq, value, batch);
     P->launches++;
     CUDA_TRY(cudaGetLastError());
