@@ -42,6 +42,30 @@ def _peaks():
         return FALLBACK_HBM, "fallback"
 
 
+FP32_PEAK_TFLOPS = 74.0  # measured: profiles/micro/ffma2_rate (packed FFMA2, B200, 1965 MHz)
+
+
+def _fp32_view(per_kernel, dom_key):
+    """FP32-pipe view of the roofline: the pass kernels are issue/FMA bound once fused, so
+    the HBM fraction alone under-states how busy they are. achieved = executed FP32 flops of
+    the launches (per-row counts from ncu source counters) / their CUDA-event time."""
+    def one(v):
+        if v.get("flops_missing") or not v.get("flops"):
+            return None
+        t = v["flops"] / (v["ms"] / 1e3) / 1e12
+        return {"achieved": round(t, 2), "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": round(t / FP32_PEAK_TFLOPS, 4)}
+    dom = one(per_kernel[dom_key])
+    if dom is None:
+        return None
+    tot = {"flops": sum(v.get("flops", 0.0) for v in per_kernel.values()),
+           "ms": sum(v["ms"] for v in per_kernel.values()),
+           "flops_missing": any(v.get("flops_missing") for v in per_kernel.values())}
+    return {"kernel": dom_key, **dom, "all_pass_kernels": one(tot),
+            "peak_source": "profiles/micro/ffma2_rate.cu (measured)",
+            "flops_source": "profiles/ncu_fp32.json (ncu source counters, executed FFMA2/FMUL2/FFMA/FMUL/FADD)"}
+
+
 def _dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -289,6 +313,10 @@ def run_ours(args, world, rank, local):
         tile_choice = {"rows": prow, "ms": {str(m): round(v.mean_seconds * 1e3, 3) for m, v in st.items()}}
         plan = plan_for_tile_bits(wl.circuit, b, M_best)
         args.M = M_best
+    else:
+        from paper_2506_04891_b200.planner import plan_for_tile_bits
+
+        plan = plan_for_tile_bits(wl.circuit, b, args.M)  # the e2e leg compiles the same tiling
     eng = Engine(wl.circuit, device=dev, M=args.M, R=args.R)
     theta = torch.as_tensor(wl.theta, device=dev)
     x = torch.as_tensor(wl.x[r0:r1], device=dev)
@@ -344,6 +372,13 @@ def run_ours(args, world, rank, local):
     eng.native.set_profiling(True)
     per_kernel = {}
     nprof = max(2, min(args.steps, 5))
+    # executed FP32 flops per row of each pass kernel, from ncu source counters of the same
+    # kernels (profiles/ncu_fp32.py); the launch times below are this run's own CUDA events
+    fp32_key = f"cfg{cfg}_M{eng.program.passes[0].M}_R{eng.program.passes[0].R}"
+    try:
+        fp32_tab = json.load(open(os.path.join(ROOT, "profiles", "ncu_fp32.json")))
+    except Exception:
+        fp32_tab = {}
     for _ in range(nprof):
         eng.native.profile = []
         eng.fwd_bwd(theta, x, batch=b, weights=w, rows=False, encoding_grads=False, micro_batch=mb,
@@ -356,6 +391,11 @@ def run_ours(args, world, rank, local):
             d["bytes"] += vec * rows_launch * (8 << n)
             d["ms"] += t
             d["launches"] += 1
+            fl = fp32_tab.get(f"{fp32_key}|lsq_jit_p{pidx}_m{mode}", {}).get("flops_per_row")
+            if fl is not None and eng.variant == "jit":
+                d["flops"] = d.get("flops", 0.0) + fl * rows_launch
+            else:
+                d["flops_missing"] = True
     eng.native.set_profiling(False)
     peak, peak_src = _peaks()
     dom = max(per_kernel.items(), key=lambda kv: kv[1]["ms"])
@@ -377,6 +417,7 @@ def run_ours(args, world, rank, local):
         "all_pass_kernels": {"achieved": round(all_b / (all_ms / 1e3) / 1e9, 1),
                              "frac": round(all_b / (all_ms / 1e3) / 1e9 / peak, 4),
                              "share_of_step": round((all_ms / nprof) / (ms / args.steps), 4)},
+        "fp32": _fp32_view(per_kernel, dom[0]),
         "per_kernel": {k: {"GBps": round(v["bytes"] / (v["ms"] / 1e3) / 1e9, 1),
                            "ms_per_step": v["ms"] / nprof,
                            "launches_per_step": v["launches"] // nprof}
@@ -392,7 +433,10 @@ def run_ours(args, world, rank, local):
     barrier()
     t0 = time.perf_counter()
     for _ in range(args.steps):
+        tq = time.perf_counter()
         res = gradient(wl.circuit, wl.theta, x_host, batch=b, weights=wl.weights, device=dev, plan=plan)
+        if os.environ.get("LSQ_E2E_TRACE") == "1":
+            print(f"gradient(): {1e3 * (time.perf_counter() - tq):.3f} ms", file=sys.stderr)
         if world > 1:
             import torch.distributed as dist
 

@@ -11,6 +11,8 @@ from __future__ import annotations
 
 import ctypes
 import os
+import sys
+import time
 
 import numpy as np
 import torch
@@ -371,6 +373,9 @@ class Engine:
                 "encoding_grads": erows[:, : self.E]}
 
 
+_TRACE = os.environ.get("LSQ_E2E_TRACE") == "1"
+
+
 class GradStep:
     """Static-buffer forward+adjoint step captured in a CUDA graph.
 
@@ -462,15 +467,23 @@ class GradStep:
         if w is not None:
             hi[nT + self.batch * nE :] = np.asarray(w, dtype=np.float64).reshape(-1)
         stream = torch.cuda.current_stream(e.device)
+        t0 = time.perf_counter() if _TRACE else 0.0
         self.d_in.copy_(self.h_in, non_blocking=True)
         if self.graph is not None:
             self.graph.replay()
         else:
             self.out = self._call()
         self.h_out.copy_(self.d_out, non_blocking=True)
+        t1 = time.perf_counter() if _TRACE else 0.0
         stream.synchronize()
+        t2 = time.perf_counter() if _TRACE else 0.0
         ho = self.h_out.numpy()
-        return {k: ho[o : o + int(np.prod(sh))].reshape(sh).copy() for k, (o, sh) in self.out_views.items()}
+        out = {k: ho[o : o + int(np.prod(sh))].reshape(sh).copy() for k, (o, sh) in self.out_views.items()}
+        if _TRACE:
+            t3 = time.perf_counter()
+            print(f"run_host: launch {1e3 * (t1 - t0):.3f} ms, wait {1e3 * (t2 - t1):.3f} ms, "
+                  f"unpack {1e3 * (t3 - t2):.3f} ms", file=sys.stderr)
+        return out
 
 
 _CACHE: "OrderedDict" = None
