@@ -712,6 +712,34 @@ def _emit_exchange(w, P, a, b, nv):
             w(f"v[{q}][{i}] = s_x[sx{b} ^ {P.soff(b, i)}u];")
 
 
+class _Rot:
+    """Exchange buffers of the adjoint and turnaround kernels: the exchange buffer and the two
+    prefetch-stage vectors (the next tile is prefetched only after the last exchange, so the
+    stage is free while a tile is transposed). A buffer read since the last barrier is
+    "dirty"; an exchange writes clean buffers first and pays a barrier only when it must
+    reuse a dirty one, so a two-vector exchange costs two barriers instead of four and a
+    one-vector exchange one instead of two."""
+
+    def __init__(self, P):
+        self.bufs = ["s_x", "s_stage", f"(s_stage + {1 << P.M})"]
+        self.dirty = set()
+
+    def exchange(self, w, P, a, b, vecs):
+        order = [x for x in self.bufs if x not in self.dirty] + [x for x in self.bufs if x in self.dirty]
+        use = order[: len(vecs)]
+        for q, buf in zip(vecs, use):
+            if buf in self.dirty:
+                w("__syncthreads();")
+                self.dirty = set()
+            for i in range(P.NR):
+                w(f"{buf}[sx{a} ^ {P.soff(a, i)}u] = v[{q}][{i}];")
+        w("__syncthreads();")
+        for q, buf in zip(vecs, use):
+            for i in range(P.NR):
+                w(f"v[{q}][{i}] = {buf}[sx{b} ^ {P.soff(b, i)}u];")
+        self.dirty = set(use)
+
+
 SMEM_LIMIT = 227 * 1024
 
 
@@ -750,8 +778,13 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
     nv = 1 if mode == MODE_FWD else 2
     prefetch = stage_vectors(prog, pi, mode) > 0
     nph = len(P.pp.phases)
+    # rotating exchange buffers (late next-tile prefetch) for the adjoint kernels: measured +2%
+    # there; the turnaround keeps its early prefetch (its forward half would lose the overlap)
+    rot = _Rot(P) if (prefetch and mode == MODE_BWD and nph > 1 and os.environ.get("LSQ_ROT", "1") != "0") else None
     est_regs = 2 * P.NR * nv + 40
     minb = max(1, min(4, 65536 // (P.NT * est_regs)))
+    if os.environ.get("LSQ_MINB_FWD") and mode == MODE_FWD:
+        minb = int(os.environ["LSQ_MINB_FWD"])
     matf = P.enc["matf"]
     slotf = P.enc["slotf"]
     w = _W()
@@ -878,7 +911,13 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
         """wait for this tile's prefetch, move it to registers (layout k), prefetch the next;
         without a stage (shared memory too small): direct streaming loads in layout k"""
         w.block("if (do_load)")
-        if prefetch:
+        if prefetch and rot is not None:
+            # the next tile is prefetched after the last exchange (emit_late_issue)
+            w("cp_async_wait_all();")
+            w("__syncthreads();")
+            emit_stage_read(k)
+            rot.dirty = set(rot.bufs[1:])  # stage vectors read without a barrier
+        elif prefetch:
             w("cp_async_wait_all();")
             w("__syncthreads();")
             emit_stage_read(k)
@@ -1051,10 +1090,14 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
         w("}")
 
     def emit_fwd_phases(end):
+        # forward phases carry psi only (the turnaround's lambda is formed after them)
         for k in range(end + 1):
-            _emit_ops(w, P, k, False, nv)
+            _emit_ops(w, P, k, False, 1)
             if k < end:
-                _emit_exchange(w, P, k, k + 1, nv)
+                if rot is not None:
+                    rot.exchange(w, P, k, k + 1, [0])
+                else:
+                    _emit_exchange(w, P, k, k + 1, 1)
 
     obs = getattr(prog, "obs", None) if mode == MODE_TURN else None
 
@@ -1197,11 +1240,27 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
         w.ind -= 1
         w("}")
 
+    def emit_late_issue():
+        """rot mode: every thread is past its last read of the stage -> prefetch tile t + 1"""
+        w("__syncthreads();")
+        rot.dirty = set()
+        w.block("if (do_load && t + 1 < t_end)")
+        emit_issue("t + 1")
+        w.end()
+        w("cp_async_commit();")
+
     def emit_bwd_phases():
+        if rot is not None and top == 0:
+            emit_late_issue()
         for k in range(top, -1, -1):
             _emit_ops(w, P, k, True, nv)
             if k > 0:
-                _emit_exchange(w, P, k, k - 1, nv)
+                if rot is not None:
+                    rot.exchange(w, P, k, k - 1, list(range(nv)))
+                    if k == 1:
+                        emit_late_issue()
+                else:
+                    _emit_exchange(w, P, k, k - 1, nv)
         P.coup.flush(w)
 
     def emit_store(k, what):
@@ -1235,9 +1294,13 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
         emit_store(0, "lam")
     else:
         # turnaround: forward phases (unless NOFWD), <Z>, lambda = O psi, adjoint phases
+        d0 = set(rot.dirty) if rot is not None else None
         w.block("if (nofwd)")
         emit_load(top)
         w.end()
+        d1 = set(rot.dirty) if rot is not None else None
+        if rot is not None:
+            rot.dirty = set(d0)
         w.block("else")
         w.block("if (do_load)")
         emit_load(0)
@@ -1247,6 +1310,8 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
         w.end()
         emit_fwd_phases(top)
         w.end()
+        if rot is not None:
+            rot.dirty |= d1  # either branch may have run
         emit_zpart(top)
         emit_lambda_init(top)
         emit_bwd_phases()
