@@ -720,8 +720,8 @@ class _Rot:
     reuse a dirty one, so a two-vector exchange costs two barriers instead of four and a
     one-vector exchange one instead of two."""
 
-    def __init__(self, P):
-        self.bufs = ["s_x", "s_stage", f"(s_stage + {1 << P.M})"]
+    def __init__(self, P, nstage):
+        self.bufs = ["s_x", "s_stage", f"(s_stage + {1 << P.M})"][: 1 + nstage]
         self.dirty = set()
 
     def exchange(self, w, P, a, b, vecs):
@@ -780,7 +780,14 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
     nph = len(P.pp.phases)
     # rotating exchange buffers (late next-tile prefetch) for the adjoint kernels: measured +2%
     # there; the turnaround keeps its early prefetch (its forward half would lose the overlap)
-    rot = _Rot(P) if (prefetch and mode == MODE_BWD and nph > 1 and os.environ.get("LSQ_ROT", "1") != "0") else None
+    rot = None
+    if prefetch and os.environ.get("LSQ_ROT", "1") != "0":
+        if mode == MODE_BWD and nph > 1:
+            rot = _Rot(P, 2)
+        elif mode == MODE_FWD and nph >= int(os.environ.get("LSQ_ROT_FWD_PHASES", "99")):
+            # forward kernels: measured neutral (one vector: the early prefetch overlap matters
+            # as much as the saved barrier), so off by default
+            rot = _Rot(P, 1)
     est_regs = 2 * P.NR * nv + 40
     minb = max(1, min(4, 65536 // (P.NT * est_regs)))
     if os.environ.get("LSQ_MINB_FWD") and mode == MODE_FWD:
@@ -1096,6 +1103,8 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
             if k < end:
                 if rot is not None:
                     rot.exchange(w, P, k, k + 1, [0])
+                    if k == end - 1 and mode == MODE_FWD:
+                        emit_late_issue()
                 else:
                     _emit_exchange(w, P, k, k + 1, 1)
 
