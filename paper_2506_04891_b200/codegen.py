@@ -702,14 +702,47 @@ def _emit_ops(w, P, ph_idx, mode_bwd, nv):
             _emit_drun(w, P, op, ph_idx, mode_bwd, nv)
 
 
+def _pairs(P, ph):
+    """Register pairs (i, j) held at adjacent local positions (local bit 0 is register bit k0):
+    one 16-byte shared access moves both; None when local bit 0 is a thread bit."""
+    regs = P.pp.phases[ph].regs
+    if not VEC_SMEM or 0 not in regs:
+        return None
+    k0 = regs.index(0)
+    return [(i, i | (1 << k0)) for i in range(P.NR) if not (i >> k0) & 1]
+
+
+def _emit_put(w, P, buf, a, q):
+    """vector q (registers, layout a) -> buf (swizzled)"""
+    pr = _pairs(P, a)
+    if pr is None:
+        for i in range(P.NR):
+            w(f"{buf}[sx{a} ^ {P.soff(a, i)}u] = v[{q}][{i}];")
+    else:
+        for i, j in pr:
+            w(f"st_pair({buf}, sx{a} ^ {P.soff(a, i)}u, v[{q}][{i}], v[{q}][{j}]);")
+
+
+def _emit_get(w, P, buf, b, q):
+    """buf (swizzled) -> vector q (registers, layout b)"""
+    pr = _pairs(P, b)
+    if pr is None:
+        for i in range(P.NR):
+            w(f"v[{q}][{i}] = {buf}[sx{b} ^ {P.soff(b, i)}u];")
+    else:
+        for i, j in pr:
+            w(f"ld_pair({buf}, sx{b} ^ {P.soff(b, i)}u, v[{q}][{i}], v[{q}][{j}]);")
+
+
+VEC_SMEM = os.environ.get("LSQ_VEC_SMEM", "1") != "0"
+
+
 def _emit_exchange(w, P, a, b, nv):
     for q in range(nv):
         w("__syncthreads();")
-        for i in range(P.NR):
-            w(f"s_x[sx{a} ^ {P.soff(a, i)}u] = v[{q}][{i}];")
+        _emit_put(w, P, "s_x", a, q)
         w("__syncthreads();")
-        for i in range(P.NR):
-            w(f"v[{q}][{i}] = s_x[sx{b} ^ {P.soff(b, i)}u];")
+        _emit_get(w, P, "s_x", b, q)
 
 
 class _Rot:
@@ -731,12 +764,10 @@ class _Rot:
             if buf in self.dirty:
                 w("__syncthreads();")
                 self.dirty = set()
-            for i in range(P.NR):
-                w(f"{buf}[sx{a} ^ {P.soff(a, i)}u] = v[{q}][{i}];")
+            _emit_put(w, P, buf, a, q)
         w("__syncthreads();")
         for q, buf in zip(vecs, use):
-            for i in range(P.NR):
-                w(f"v[{q}][{i}] = {buf}[sx{b} ^ {P.soff(b, i)}u];")
+            _emit_get(w, P, buf, b, q)
         self.dirty = set(use)
 
 
@@ -894,7 +925,13 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
 
     def emit_stage_read(k):
         ph = P.pp.phases[k]
+        pr = _pairs(P, k)
         for vi, _ in ld_vecs:
+            if pr is not None:  # natural order: the pair on local bit 0 is adjacent
+                for i, j in pr:
+                    loc = sum(1 << ph.regs[b] for b in range(P.R) if (i >> b) & 1)
+                    w(f"ld_pair(s_stage, {vi * (1 << P.M)} + (tp{k} | {loc}u), v[{vi}][{i}], v[{vi}][{j}]);")
+                continue
             for i in range(P.NR):
                 loc = sum(1 << ph.regs[b] for b in range(P.R) if (i >> b) & 1)
                 w(f"v[{vi}][{i}] = s_stage[{vi * (1 << P.M)} + (tp{k} | {loc}u)];")

@@ -417,8 +417,10 @@ def schedule_passes(groups, n, M, seeds: int = 12, skip=()) -> list[PassPlan]:
 
 # ----------------------------------------------------------------------------- phases
 
-# Shared-memory XOR swizzle of the amplitude index: S(L) = L ^ h(L >> 4), h linear.
-SWZ_H = [1, 2, 4, 8, 3, 6, 12, 11, 5, 10, 7, 14, 15, 9]
+# Shared-memory XOR swizzle of the amplitude index: S(L) = L ^ h(L >> 4), h linear into local
+# bits 1..3 only. Bit 0 is never swizzled, so the two amplitudes of a register pair on local
+# bit 0 stay adjacent and 16-byte aligned: one 16 B shared access moves both.
+SWZ_H = [2, 4, 8, 6, 12, 10, 14, 2, 4, 8, 6, 12, 10, 14]
 
 
 def swz_vec(local_bit: int) -> int:
@@ -429,16 +431,21 @@ def swz_vec(local_bit: int) -> int:
 
 
 def _lane_order(thread_bits, coalesced):
-    """Order thread bits so the 4 lowest lanes' swizzle vectors are independent."""
+    """Order thread bits so the lowest lanes hit distinct banks: with 8-byte accesses (local bit
+    0 on a lane) bit 0 leads and three lanes independent over swizzle bits 1..3 follow; with
+    16-byte pair accesses (local bit 0 in registers) the first three lanes are independent."""
     tb = sorted(thread_bits)
     if coalesced:
         return tb  # local bits 0..3 first: contiguous 128 B per half-warp
     chosen, basis = [], []
     rest = list(tb)
-    for b in tb:
+    if 0 in rest:
+        chosen.append(0)
+        rest.remove(0)
+    for b in list(rest):
         if len(chosen) == 4:
             break
-        v = swz_vec(b)
+        v = swz_vec(b) & 14
         for e in basis:
             v = min(v, v ^ e)
         if v:
