@@ -753,8 +753,14 @@ class _Rot:
     reuse a dirty one, so a two-vector exchange costs two barriers instead of four and a
     one-vector exchange one instead of two."""
 
-    def __init__(self, P, nstage):
-        self.bufs = ["s_x", "s_stage", f"(s_stage + {1 << P.M})"][: 1 + nstage]
+    def __init__(self, P, nstage, late=True):
+        # late: the stage is free during the tile (prefetch issued after the last transpose);
+        # otherwise only the stage's unused second vector (turnaround kernels) joins s_x
+        self.late = late
+        if late:
+            self.bufs = ["s_x", "s_stage", f"(s_stage + {1 << P.M})"][: 1 + nstage]
+        else:
+            self.bufs = ["s_x", f"(s_stage + {1 << P.M})"]
         self.dirty = set()
 
     def exchange(self, w, P, a, b, vecs):
@@ -815,6 +821,8 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
     if prefetch and os.environ.get("LSQ_ROT", "1") != "0":
         if mode == MODE_BWD and nph > 1:
             rot = _Rot(P, 2)
+        elif mode == MODE_TURN and nph > 1 and os.environ.get("LSQ_ROT_TURN", "1") != "0":
+            rot = _Rot(P, 2, late=False)  # psi-only stage: its lambda half is a spare buffer
         elif mode == MODE_FWD and nph >= int(os.environ.get("LSQ_ROT_FWD_PHASES", "99")):
             # forward kernels: measured neutral (one vector: the early prefetch overlap matters
             # as much as the saved barrier), so off by default
@@ -942,6 +950,9 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
         w.end()
         w("cp_async_commit();")
     w.block("for (int t = t0; t < t_end; ++t)")
+    if rot is not None and not rot.late:
+        # previous tile's last transpose may still be read: the first write here syncs first
+        rot.dirty = set(rot.bufs)
     tb = [f"((uint64_t)((t >> {j}) & 1)) << {p}" for j, p in enumerate(P.nbit)]
     w(f"const uint64_t tbase = {' | '.join(tb) if tb else '0ull'};")
     # opaque per-tile copies of the shared-memory thread offsets: keeps the 2^R swizzled
@@ -955,7 +966,7 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
         """wait for this tile's prefetch, move it to registers (layout k), prefetch the next;
         without a stage (shared memory too small): direct streaming loads in layout k"""
         w.block("if (do_load)")
-        if prefetch and rot is not None:
+        if prefetch and rot is not None and rot.late:
             # the next tile is prefetched after the last exchange (emit_late_issue)
             w("cp_async_wait_all();")
             w("__syncthreads();")
@@ -1140,7 +1151,7 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
             if k < end:
                 if rot is not None:
                     rot.exchange(w, P, k, k + 1, [0])
-                    if k == end - 1 and mode == MODE_FWD:
+                    if k == end - 1 and mode == MODE_FWD and rot.late:
                         emit_late_issue()
                 else:
                     _emit_exchange(w, P, k, k + 1, 1)
@@ -1296,14 +1307,14 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
         w("cp_async_commit();")
 
     def emit_bwd_phases():
-        if rot is not None and top == 0:
+        if rot is not None and rot.late and top == 0:
             emit_late_issue()
         for k in range(top, -1, -1):
             _emit_ops(w, P, k, True, nv)
             if k > 0:
                 if rot is not None:
                     rot.exchange(w, P, k, k - 1, list(range(nv)))
-                    if k == 1:
+                    if k == 1 and rot.late:
                         emit_late_issue()
                 else:
                     _emit_exchange(w, P, k, k - 1, nv)
