@@ -1345,10 +1345,11 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
     elif mode == MODE_BWD:
         emit_load(top)
         emit_bwd_phases()
-        if use_prefix:
-            emit_prefix_lambda(0)
+        # stores first: psi is dead before the prefix-boundary couplings (which read lambda only)
         emit_store(0, "psi")
         emit_store(0, "lam")
+        if use_prefix:
+            emit_prefix_lambda(0)
     else:
         # turnaround: forward phases (unless NOFWD), <Z>, lambda = O psi, adjoint phases
         d0 = set(rot.dirty) if rot is not None else None
@@ -1372,10 +1373,10 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
         emit_zpart(top)
         emit_lambda_init(top)
         emit_bwd_phases()
-        if use_prefix and len(prog.passes) == 1:
-            emit_prefix_lambda(0)
         emit_store(0, "psi")
         emit_store(0, "lam")
+        if use_prefix and len(prog.passes) == 1:
+            emit_prefix_lambda(0)
     w.end()  # tile loop
     # flush partials
     w("__syncthreads();")
