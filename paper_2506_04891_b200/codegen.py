@@ -557,12 +557,14 @@ def _emit_drun_walsh(w, P, subs, tp):
         free = [slot + q for q in range(2 << ar) if slot + q not in used]
         P.coup.add(w, nm, slot + 2 * c - 1, free)
 
-def _emit_drun(w, P, op, ph_idx, mode_bwd, nv):
+def _emit_drun(w, P, op, ph_idx, mode_bwd, nv, couplings=True, rotate=True):
     subs = P.enc["subs"][op[6] : op[6] + op[7]]
     tp = f"tp{ph_idx}"
     R = P.R
     # couplings (backward, before un-applying: conj(l) p is phase invariant)
-    if mode_bwd and any(int(s[4]) >= 0 for s in subs) and P.walsh_diag:
+    if not couplings:
+        pass
+    elif mode_bwd and any(int(s[4]) >= 0 for s in subs) and P.walsh_diag:
         _emit_drun_walsh(w, P, subs, tp)
     elif mode_bwd and any(int(s[4]) >= 0 for s in subs):
         names = {si: [P.coup.new(w) for _ in range(1 << int(s[5]))] for si, s in enumerate(subs) if int(s[4]) >= 0}
@@ -616,8 +618,25 @@ def _emit_drun(w, P, op, ph_idx, mode_bwd, nv):
                 for e in range(ne):
                     P.coup.add(w, names[si][e], slot + 2 * e + 1, free)
     # phases
+    if not rotate:
+        return
     w("{")
     w.ind += 1
+    per_i = _drun_prelude(w, P, subs, tp)
+    inv = "true" if mode_bwd else "false"
+    for i in range(P.NR):
+        expr = " + ".join(["cph"] + per_i[i])
+        w(f"{{ const int32_t p_ = {expr};")
+        for q in range(nv):
+            w(f"  v[{q}][{i}] = phase_rot(v[{q}][{i}], p_, {inv});")
+        w("}")
+    w.ind -= 1
+    w("}")
+
+
+def _drun_prelude(w, P, subs, tp):
+    """Emit the run's thread-constant phase cph and table pointers in the current scope;
+    return the per-register-index phase terms."""
     w("int32_t cph = 0;")
     per_i = [[] for _ in range(P.NR)]
     for si, s in enumerate(subs):
@@ -646,13 +665,74 @@ def _emit_drun(w, P, op, ph_idx, mode_bwd, nv):
                 w(f"const int32_t lo{si} = a{si}[2 * {ea}], hi{si} = a{si}[2 * {ea} + 1];")
                 for i in range(P.NR):
                     per_i[i].append(f"{'hi' if (i >> eb) & 1 else 'lo'}{si}")
-    inv = "true" if mode_bwd else "false"
+    return per_i
+
+
+FOLD_DRUN = os.environ.get("LSQ_FOLD_DRUN", "1") != "0"
+FOLD_MAXC = int(os.environ.get("LSQ_FOLD_MAXC", "2"))
+FOLD_FWD = os.environ.get("LSQ_FOLD_FWD", "1") != "0"
+
+
+def _fold_classes(P, op, ph_idx, k):
+    """Pairs (i, i | 2^k) of a diagonal run followed by a one-qubit group on register bit k,
+    grouped by their (phase_i, phase_j) term lists; None when the run has more than FOLD_MAXC
+    classes (then rotating every amplitude is cheaper)."""
+    subs = P.enc["subs"][op[6] : op[6] + op[7]]
+    tp = f"tp{ph_idx}"
+    w0 = _W()
+    per_i = _drun_prelude(w0, P, subs, tp)
+    cls = {}
     for i in range(P.NR):
-        expr = " + ".join(["cph"] + per_i[i])
-        w(f"{{ const int32_t p_ = {expr};")
-        for q in range(nv):
-            w(f"  v[{q}][{i}] = phase_rot(v[{q}][{i}], p_, {inv});")
-        w("}")
+        if (i >> k) & 1:
+            continue
+        j = i | (1 << k)
+        cls.setdefault((tuple(per_i[i]), tuple(per_i[j])), []).append((i, j))
+    return cls if len(cls) <= FOLD_MAXC else None
+
+
+def _emit_fold(w, P, dop, uop, ph_idx, mode_bwd, nv):
+    """Diagonal run D followed by a one-qubit group U on register bit k, applied as one op:
+    forward U D (columns of U scaled by the run's phase of each pair member), adjoint
+    (U D)^+ = D^+ U^+ (rows of U^+ scaled by the conjugate phases). One coefficient set per
+    class of pairs (FOLD_MAXC at most) instead of a phase rotation of every amplitude of every
+    vector; the run's couplings (conj(lam) psi is phase invariant) are taken after."""
+    k = int(uop[1])
+    moff = int(uop[5])
+    subs = P.enc["subs"][dop[6] : dop[6] + dop[7]]
+    tp = f"tp{ph_idx}"
+    w("{")
+    w.ind += 1
+    per_i = _drun_prelude(w, P, subs, tp)
+    w(f"const float* g_ = s_mat + {moff};")
+    # U entries as complex pairs (row-major)
+    w("const float2 u00_ = make_float2(g_[0], g_[1]), u01_ = make_float2(g_[2], g_[3]), "
+      "u10_ = make_float2(g_[4], g_[5]), u11_ = make_float2(g_[6], g_[7]);")
+    cls = {}
+    for i in range(P.NR):
+        if (i >> k) & 1:
+            continue
+        j = i | (1 << k)
+        cls.setdefault((tuple(per_i[i]), tuple(per_i[j])), []).append((i, j))
+    for c, ((ti, tj), pairs) in enumerate(cls.items()):
+        ei = " + ".join(["cph"] + list(ti))
+        ej = " + ".join(["cph"] + list(tj))
+        w(f"const float2 pi{c}_ = phase_cs({ei}), pj{c}_ = phase_cs({ej});")
+        if not mode_bwd:  # W = U diag(p_i, p_j)
+            ent = [("u00_", f"pi{c}_"), ("u01_", f"pj{c}_"), ("u10_", f"pi{c}_"), ("u11_", f"pj{c}_")]
+        else:  # W = diag(p_i, p_j)^* U^+: W_ab = conj(U_ba p_a)
+            ent = [("u00_", f"pi{c}_"), ("u10_", f"pi{c}_"), ("u01_", f"pj{c}_"), ("u11_", f"pj{c}_")]
+        for e, (u, ph) in enumerate(ent):
+            w(f"const float2 t{c}_{e} = cm({ph}.x, {ph}.y, {u});")
+        conj = "-" if mode_bwd else ""
+        w(f"const float f{c}_[8] = {{" + ", ".join(f"t{c}_{e}.x, {conj}t{c}_{e}.y" for e in range(4)) + "};")
+        for q in range(nv if mode_bwd else 1):
+            for i, j in pairs:
+                w(f"{{ const float2 x0 = v[{q}][{i}], x1 = v[{q}][{j}];")
+                for a, dst in ((0, i), (1, j)):
+                    e0, e1 = 2 * a, 2 * a + 1
+                    w(f"  v[{q}][{dst}] = fix(x1, f{c}_[{2 * e1 + 1}], fx(x1, f{c}_[{2 * e1}], "
+                      f"fix(x0, f{c}_[{2 * e0 + 1}], mx(x0, f{c}_[{2 * e0}]))));")
+                w("}")
     w.ind -= 1
     w("}")
 
@@ -661,8 +741,38 @@ def _emit_ops(w, P, ph_idx, mode_bwd, nv):
     ops = P.enc["ops"][ph_idx]
     seq = list(reversed(ops)) if mode_bwd else ops
     regs = P.pp.phases[ph_idx].regs
-    for op in seq:
+
+    def foldable(dop, uop):
+        if not FOLD_DRUN or dop is None or uop is None:
+            return False
+        if int(dop[0]) != S.OP_DRUN or int(uop[0]) != S.OP_U1:
+            return False
+        grp = P.prog.groups[int(uop[3])]
+        if _group_const_matrix(grp, P.drop_phase) is not None:
+            return False
+        if any(c != "c" for row in u1_structure(grp)[0] for c in row):
+            return False  # structured (real / sparse) groups would lose their cheap apply
+        return _fold_classes(P, dop, ph_idx, int(uop[1])) is not None
+
+    skip = False
+    for idx, op in enumerate(seq):
+        if skip:
+            skip = False
+            continue
         kind = int(op[0])
+        nxt = seq[idx + 1] if idx + 1 < len(seq) else None
+        if not mode_bwd and FOLD_FWD and kind == S.OP_DRUN and foldable(op, nxt):
+            _emit_fold(w, P, op, nxt, ph_idx, False, nv)
+            skip = True
+            continue
+        if mode_bwd and kind == S.OP_U1 and foldable(nxt, op):
+            slot = int(op[4])
+            if slot >= 0:
+                _emit_u1_coupling(w, P, int(op[1]), slot, u1_structure(P.prog.groups[int(op[3])])[1])
+            _emit_fold(w, P, nxt, op, ph_idx, True, nv)
+            _emit_drun(w, P, nxt, ph_idx, True, nv, couplings=True, rotate=False)
+            skip = True
+            continue
         if kind == S.OP_PX:
             for q in range(nv):
                 w(f"perm_x<{P.R}, {int(op[1])}>(v[{q}]);")
