@@ -293,7 +293,7 @@ def _emit_u1_coupling(w, P, k, slot, comps):
                 accs[c] = f"vm{fn}({a}, {b})" if accs[c] is None else f"vf{fn}({a}, {b}, {accs[c]})"
         for c in range(nch):
             w(f"const float2 t{ci}_{c} = {accs[c]};")
-        w(f"{names[ci]} = {_tree_sum([f't{ci}_{c}.x' for c in range(nch)] + [f't{ci}_{c}.y' for c in range(nch)])};")
+        w(f"{names[ci]} = {_scaled(P, _tree_sum([f't{ci}_{c}.x' for c in range(nch)] + [f't{ci}_{c}.y' for c in range(nch)]))};")
     w.ind -= 1
     w("}")
     used = {pos for _, pos in lay}
@@ -347,6 +347,75 @@ def _emit_small(w, v, U, q):
                     expr = f"{'fx' if kind == 'x' else 'fix'}(x{c}, {_f(coef)}, {expr})"
         w(f"  {v}[{q[r]}] = {expr if expr else 'make_float2(0.f, 0.f)'};")
     w("}")
+
+
+UNIT_CONST = os.environ.get("LSQ_UNIT_CONST", "1") != "0"
+
+
+def unit_form(U):
+    """(kappa, U / kappa) when every nonzero entry of the constant matrix U has modulus kappa
+    and U / kappa has entries in {0, +-1, +-i} (MS(0,0), ECR, H, X90 ...); else None."""
+    mags = np.abs(U[np.abs(U) > 1e-12])
+    if mags.size == 0:
+        return None
+    kappa = float(mags.max())
+    if np.any(np.abs(mags - kappa) > 1e-9 * kappa):
+        return None
+    V = U / kappa
+    ok = (np.abs(V) < 1e-12) | (np.abs(V - 1) < 1e-9) | (np.abs(V + 1) < 1e-9) | \
+         (np.abs(V - 1j) < 1e-9) | (np.abs(V + 1j) < 1e-9)
+    if not ok.all() or abs(kappa - 1.0) < 1e-12:
+        return None
+    return kappa, np.round(V.real) + 1j * np.round(V.imag)
+
+
+def _emit_unit_small(w, v, V, q):
+    """Constant matrix with entries in {0, +-1, +-i} (the scale is deferred): an output row with
+    a +1 entry starts from that amplitude (no multiply) and adds the others with one FFMA2 each
+    (coefficient +-1 on x or on i x); rows without a +1 entry fall back to one multiply."""
+    d = len(q)
+    w("{ " + " ".join(f"const float2 x{c} = {v}[{q[c]}];" for c in range(d)))
+    for r in range(d):
+        terms = [(c, complex(V[r, c])) for c in range(d) if abs(V[r, c]) > 0.5]
+        first = next((t for t in terms if abs(t[1] - 1) < 1e-9), None)
+        if first is not None:
+            expr = f"x{first[0]}"
+            rest = [t for t in terms if t is not first]
+        else:
+            c0, a = terms[0]
+            expr = f"mx(x{c0}, {_f(a.real)})" if abs(a.imag) < 0.5 else f"mulix(x{c0}, {_f(a.imag)})"
+            rest = terms[1:]
+        for c, a in rest:
+            if abs(a.imag) < 0.5:
+                expr = f"fx(x{c}, {_f(a.real)}, {expr})"
+            else:
+                expr = f"fix(x{c}, {_f(a.imag)}, {expr})"
+        w(f"  {v}[{q[r]}] = {expr if terms else 'make_float2(0.f, 0.f)'};")
+    w("}")
+
+
+def _emit_unit_const(w, P, v, V, regs_bits, dagger):
+    if dagger:
+        V = np.conj(V.T)
+    R = P.R
+    if V.shape[0] == 2:
+        (k,) = regs_bits
+        for i in range(1 << R):
+            if not (i >> k) & 1:
+                _emit_unit_small(w, v, V, [i, i | (1 << k)])
+    else:
+        ka, kb = regs_bits
+        for i in range(1 << R):
+            if not ((i >> ka) & 1) and not ((i >> kb) & 1):
+                _emit_unit_small(w, v, V, [i, i | (1 << kb), i | (1 << ka), i | (1 << ka) | (1 << kb)])
+
+
+def _scaled(P, expr, q=(0, 1)):
+    """expr times 1 / prod of the deferred scales of the vectors in q (1: no multiply)."""
+    c = 1.0
+    for i in q:
+        c /= P.sc[i]
+    return expr if abs(c - 1.0) < 1e-15 else f"(({expr}) * {_f(c)})"
 
 
 def _src_expr(sw, P, tp_var):
@@ -543,7 +612,7 @@ def _emit_drun_walsh(w, P, subs, tp):
             accs[c] = f"vm{fn}(v[1][{i}], v[0][{i}])" if accs[c] is None else f"vf{fn}(v[1][{i}], v[0][{i}], {accs[c]})"
         for c in range(nch):
             w(f"const float2 wt{m}_{c} = {accs[c]};")
-        w(f"const float wv{m} = {_tree_sum([f'wt{m}_{c}.x' for c in range(nch)] + [f'wt{m}_{c}.y' for c in range(nch)])};")
+        w(f"const float wv{m} = {_scaled(P, _tree_sum([f'wt{m}_{c}.x' for c in range(nch)] + [f'wt{m}_{c}.y' for c in range(nch)]))};")
     for (si, slot, ar, c, regmask, signs), nm in zip(plan, names):
         if signs:
             par = " ^ ".join(f"(int)({e})" for e in signs)
@@ -788,12 +857,21 @@ def _emit_ops(w, P, ph_idx, mode_bwd, nv):
                 if kind == S.OP_U1:
                     _emit_u1_coupling(w, P, bits[0], slot, u1_structure(grp)[1])
                 else:
+                    csc = _scaled(P, "1.f")
+                    fix_ = "" if csc == "1.f" else f"for (int e_ = 0; e_ < 8; ++e_) acc[e_] *= {csc}; "
                     for rr in range(4):
                         w(f"{{ float acc[8] = {{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}}; "
-                          f"u2_coupling_row<{P.R}, {bits[0]}, {bits[1]}, {rr}>(v[0], v[1], acc); "
+                          f"u2_coupling_row<{P.R}, {bits[0]}, {bits[1]}, {rr}>(v[0], v[1], acc); {fix_}"
                           f"warp_accumulate8<{P.NT}>(acc, wacc + {slot + 8 * rr}); }}")
             U = _group_const_matrix(grp, P.drop_phase)
-            if U is not None:
+            uf = unit_form(U) if (U is not None and UNIT_CONST and P.walsh_diag) else None
+            if uf is not None:
+                # U / kappa with entries in {0, +-1, +-i}; the vectors carry the deferred scale
+                kappa, V = uf
+                for q in range(nv if mode_bwd else 1):
+                    _emit_unit_const(w, P, f"v[{q}]", V, bits, mode_bwd)
+                    P.sc[q] /= kappa
+            elif U is not None:
                 for q in range(nv):
                     _emit_const_u(w, P, f"v[{q}]", U, bits, mode_bwd)
             elif kind == S.OP_U1:
@@ -921,6 +999,7 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
     P.drop_phase = bool(getattr(prog, "drop_phase", False))
     P.walsh_diag = os.environ.get("LSQ_WALSH_DIAG", "1") != "0"
     P.walsh = []  # (slot, arity, components) of diagonal couplings kept as Walsh sums
+    P.sc = [1.0, 1.0]  # deferred (compile-time) scale of psi and lambda: computed = true x sc
     P.slotf = prog.enc[pi]["slotf"]
     nv = 1 if mode == MODE_FWD else 2
     prefetch = stage_vectors(prog, pi, mode) > 0
@@ -1304,6 +1383,7 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
         emit_obs_signs(k)
         emit_wht(lambda i: f"v[0][{i}].x * v[0][{i}].x + v[0][{i}].y * v[0][{i}].y", "hz_")
         vals = [f"sg{q} * hz_[{obs_parts(k, q)[0]}]" for q in range(P.n)] + ["hz_[0]"]
+        vals = [_scaled(P, v_, (0, 0)) for v_ in vals]
         offs = [P.n - 1 - q for q in range(P.n)] + [P.n]
         w("float* zw = s_zw + warp * 32;")
         npad = (-len(vals)) % 8
@@ -1335,6 +1415,7 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
         w("}")
 
     def emit_lambda_obs(k):
+        P.sc[1] = P.sc[0]  # lambda = O psi carries psi's deferred scale
         w("{")
         w.ind += 1
         emit_obs_signs(k)
@@ -1372,6 +1453,8 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
             w(f"pz[{ph.regs[kk]}] += D{kk};")
         for j, lb in enumerate(ph.threads):
             w(f"pz[{lb}] += ((tp{k} >> {lb}) & 1u) ? -S_ : S_;")
+        if _scaled(P, "1.f", (0, 0)) != "1.f":
+            w(f"for (int e_ = 0; e_ <= {P.M}; ++e_) pz[e_] *= {_scaled(P, '1.f', (0, 0))};")
         w(f"warp_sum<NT, {P.M + 1}>(pz);")
         w.block("if ((tid & 31) == 0)")
         w(f"float* zw = s_zw + warp * 32;")
@@ -1385,6 +1468,7 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
         w("}")
 
     def emit_lambda_init(k):
+        P.sc[1] = P.sc[0]  # lambda = O psi carries psi's deferred scale
         if obs:
             emit_lambda_obs(k)
             return
@@ -1431,16 +1515,29 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
         P.coup.flush(w)
 
     def emit_store(k, what):
+        q = 0 if what == "psi" else 1
+        c = 1.0 / P.sc[q]
+
+        def val(i):
+            return f"v[{q}][{i}]" if abs(c - 1.0) < 1e-15 else f"mx(v[{q}][{i}], {_f(c)})"
         if what == "psi":
             w.block("if (flags & PF_STORE_PSI)")
             for i in range(P.NR):
-                w(f"__stcs(A.psi_out + base + (gt{k} | {P.goff(k, i)}u), v[0][{i}]);")
+                w(f"__stcs(A.psi_out + base + (gt{k} | {P.goff(k, i)}u), {val(i)});")
             w.end()
         else:
             w.block("if (flags & PF_STORE_LAM)")
             for i in range(P.NR):
-                w(f"__stcs(A.lam + base + (gt{k} | {P.goff(k, i)}u), v[1][{i}]);")
+                w(f"__stcs(A.lam + base + (gt{k} | {P.goff(k, i)}u), {val(i)});")
             w.end()
+
+    def renormalize(q):
+        """bring vector q back to the true scale (a deferred scale would not survive a merge)"""
+        c = 1.0 / P.sc[q]
+        if abs(c - 1.0) > 1e-15:
+            for i in range(P.NR):
+                w(f"v[{q}][{i}] = mx(v[{q}][{i}], {_f(c)});")
+            P.sc[q] = 1.0
 
     if mode == MODE_FWD:
         emit_load(0)
@@ -1459,6 +1556,7 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
         emit_store(0, "psi")
         emit_store(0, "lam")
         if use_prefix:
+            renormalize(1)
             emit_prefix_lambda(0)
     else:
         # turnaround: forward phases (unless NOFWD), <Z>, lambda = O psi, adjoint phases
@@ -1477,6 +1575,7 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
         emit_synth(0)
         w.end()
         emit_fwd_phases(top)
+        renormalize(0)  # the nofwd branch joins with psi at scale 1
         w.end()
         if rot is not None:
             rot.dirty |= d1  # either branch may have run
@@ -1486,6 +1585,7 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
         emit_store(0, "psi")
         emit_store(0, "lam")
         if use_prefix and len(prog.passes) == 1:
+            renormalize(1)
             emit_prefix_lambda(0)
     w.end()  # tile loop
     # flush partials
