@@ -271,7 +271,7 @@ def _tree_sum(terms):
     return terms[0]
 
 
-COUPLING_CHAINS = 2  # independent partial accumulators per coupling component (ILP)
+COUPLING_CHAINS = int(os.environ.get("LSQ_COUPLING_CHAINS", "1"))  # partial sums per component: 1 measured best (registers beat ILP)
 
 
 def _emit_u1_coupling(w, P, k, slot, comps):
