@@ -900,26 +900,60 @@ def _pairs(P, ph):
     return [(i, i | (1 << k0)) for i in range(P.NR) if not (i >> k0) & 1]
 
 
+LAZY_SX = os.environ.get("LSQ_LAZY_SX", "1") != "0"
+
+
+def _has_fold(P):
+    """True when some diagonal run of the pass folds into the following one-qubit group."""
+    for ph_idx, ops in enumerate(P.enc["ops"]):
+        for a, b in zip(ops, ops[1:]):
+            if int(a[0]) != S.OP_DRUN or int(b[0]) != S.OP_U1:
+                continue
+            grp = P.prog.groups[int(b[3])]
+            if _group_const_matrix(grp, P.drop_phase) is not None:
+                continue
+            if all(c == "c" for row in u1_structure(grp)[0] for c in row) and \
+                    _fold_classes(P, a, ph_idx, int(b[1])) is not None:
+                return True
+    return False
+
+
+def _sx_open(w, k, P=None):
+    """Swizzled thread base of layout k as an opaque local copy made where it is used (one
+    LOP3 per access instead of hoisted per-register addresses; not held across the tile).
+    Measured: a gain except for adjoint kernels with folded diagonal runs (their coefficient
+    sets need the registers the early copies would otherwise free), which keep early copies."""
+    if P is not None and P.lazy_sx:
+        w(f"{{ uint32_t sxl_ = st{k}; asm volatile(\"\" : \"+r\"(sxl_));")
+        return "sxl_"
+    w("{")
+    return f"sx{k}"
+
+
 def _emit_put(w, P, buf, a, q):
     """vector q (registers, layout a) -> buf (swizzled)"""
     pr = _pairs(P, a)
+    sx = _sx_open(w, a, P)
     if pr is None:
         for i in range(P.NR):
-            w(f"{buf}[sx{a} ^ {P.soff(a, i)}u] = v[{q}][{i}];")
+            w(f"{buf}[{sx} ^ {P.soff(a, i)}u] = v[{q}][{i}];")
     else:
         for i, j in pr:
-            w(f"st_pair({buf}, sx{a} ^ {P.soff(a, i)}u, v[{q}][{i}], v[{q}][{j}]);")
+            w(f"st_pair({buf}, {sx} ^ {P.soff(a, i)}u, v[{q}][{i}], v[{q}][{j}]);")
+    w("}")
 
 
 def _emit_get(w, P, buf, b, q):
     """buf (swizzled) -> vector q (registers, layout b)"""
     pr = _pairs(P, b)
+    sx = _sx_open(w, b, P)
     if pr is None:
         for i in range(P.NR):
-            w(f"v[{q}][{i}] = {buf}[sx{b} ^ {P.soff(b, i)}u];")
+            w(f"v[{q}][{i}] = {buf}[{sx} ^ {P.soff(b, i)}u];")
     else:
         for i, j in pr:
-            w(f"ld_pair({buf}, sx{b} ^ {P.soff(b, i)}u, v[{q}][{i}], v[{q}][{j}]);")
+            w(f"ld_pair({buf}, {sx} ^ {P.soff(b, i)}u, v[{q}][{i}], v[{q}][{j}]);")
+    w("}")
 
 
 VEC_SMEM = os.environ.get("LSQ_VEC_SMEM", "1") != "0"
@@ -1146,8 +1180,10 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
     w(f"const uint64_t tbase = {' | '.join(tb) if tb else '0ull'};")
     # opaque per-tile copies of the shared-memory thread offsets: keeps the 2^R swizzled
     # exchange addresses as one LOP3 each instead of hoisted (and spilled) registers
-    for k in range(nph):
-        w(f"uint32_t sx{k} = st{k}; asm volatile(\"\" : \"+r\"(sx{k}));")
+    P.lazy_sx = LAZY_SX and not (mode == MODE_BWD and FOLD_DRUN and _has_fold(P))
+    if not P.lazy_sx:
+        for k in range(nph):
+            w(f"uint32_t sx{k} = st{k}; asm volatile(\"\" : \"+r\"(sx{k}));")
     w("const size_t base = rowbase + tbase;")
     w(f"float2 v[{nv}][{P.NR}];")
 
