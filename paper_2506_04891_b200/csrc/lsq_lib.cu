@@ -311,6 +311,15 @@ struct Geometry {
 // tpc minimises waves x (tpc + 1/2): whole waves of equal CTAs (a partial last wave leaves
 // SMs idle) against the per-CTA prologue (table staging, first tile load, partial flush),
 // costed at half a tile. Without it: about 4 CTAs per SM of 64 tiles at most.
+// per-CTA prologue cost in tiles (LSQ_GEOM_PROLOGUE overrides; A/B runs)
+double geom_prologue() {
+  static const double v = [] {
+    const char* e = getenv("LSQ_GEOM_PROLOGUE");
+    return e ? atof(e) : 0.5;
+  }();
+  return v;
+}
+
 Geometry geometry(const lsq_program* P, int pidx, int mode, int batch) {
   const PassInfo& pi = P->passes[pidx];
   const int ntiles = 1 << (P->n - pi.M);
@@ -324,7 +333,7 @@ Geometry geometry(const lsq_program* P, int pidx, int mode, int batch) {
     for (int t = std::min(ntiles, 64); t >= 1; t >>= 1) {
       const int64_t units = total / t;
       const int64_t waves = (units + G - 1) / G;
-      const double cost = (double)waves * (t + 0.5);
+      const double cost = (double)waves * (t + geom_prologue());
       if (cost < best * (1 - 1e-9)) {
         best = cost;
         best_t = t;
