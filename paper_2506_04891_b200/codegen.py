@@ -426,7 +426,6 @@ def _scaled(P, expr, q=(0, 1)):
 
 
 TAN_ROT = os.environ.get("LSQ_TAN_ROT", "1") != "0"
-TAN_FWD = os.environ.get("LSQ_TAN_FWD", "1") != "0"
 TAN_TH = 0.01  # |cos| below this: the rotation takes the two-op form
 TAN_RENORM = 8  # tangent-form rotations between forced renormalisations (range guard)
 _ROT_CACHE: dict = {}
@@ -456,13 +455,13 @@ def is_rotation(grp) -> bool:
     return ok
 
 
-def _emit_tan_rot(w, P, k, g, nvec, dagger, classes, branch=True):
+def _emit_tan_rot(w, P, k, g, nvec, dagger, classes):
     """Rotation R = [[c, -s], [s, c]] on register bit k as R / c = [[1, -t], [t, 1]]: one FFMA2
     per output amplitude instead of two; the vectors carry the run-time scale rho_ *= c
     (uniform over the block: the angle is shared or per row). |c| < TAN_TH keeps the two-op
     form (uniform branch)."""
     w(f"{{ const float c_ = {g}[0], t_ = __fdividef({g}[4], {g}[0]), nt_ = -t_;")
-    w(f"if (fabsf(c_) >= {TAN_TH}f) {{" if branch else "{")
+    w(f"if (fabsf(c_) >= {TAN_TH}f) {{")
     a0, a1 = ("t_", "nt_") if dagger else ("nt_", "t_")  # R^+/c = [[1, t], [-t, 1]]
     for q in range(nvec):
         for i in range(1 << P.R):
@@ -472,10 +471,9 @@ def _emit_tan_rot(w, P, k, g, nvec, dagger, classes, branch=True):
             w(f"  {{ const float2 x0 = v[{q}][{i}], x1 = v[{q}][{j}]; "
               f"v[{q}][{i}] = fx(x1, {a0}, x0); v[{q}][{j}] = fx(x0, {a1}, x1); }}")
     w("  rho_ *= c_;")
-    if branch:
-        w("} else {")
-        for q in range(nvec):
-            _emit_u1_struct(w, f"v[{q}]", k, P.R, classes, g, dagger)
+    w("} else {")
+    for q in range(nvec):
+        _emit_u1_struct(w, f"v[{q}]", k, P.R, classes, g, dagger)
     w("} }")
     P.rho_live = True
     P.tan_count += 1
@@ -966,12 +964,7 @@ def _emit_ops(w, P, ph_idx, mode_bwd, nv):
             elif kind == S.OP_U1:
                 classes = u1_structure(grp)[0]
                 w(f"{{ const float* g_ = s_mat + {moff};")
-                if TAN_ROT and P.tan_mode == "uncond" and is_rotation(grp):
-                    # inside a forward phase whose rotations were all checked safe up front
-                    _emit_tan_rot(w, P, bits[0], "g_", 1, False, classes, branch=False)
-                    if P.tan_count >= TAN_RENORM:
-                        _renorm_rho(w, P, 1)
-                elif TAN_ROT and P.tan_ok and is_rotation(grp):
+                if TAN_ROT and P.tan_ok and is_rotation(grp):
                     _emit_tan_rot(w, P, bits[0], "g_", nv if mode_bwd else 1, mode_bwd, classes)
                     if P.tan_count >= TAN_RENORM:
                         _renorm_rho(w, P, nv if mode_bwd else 1)
@@ -1138,7 +1131,6 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
     # tangent-form rotations in the adjoint kernels only: measured -2% there, +3% in the forward
     # and turnaround kernels (the uniform fallback branch costs them their scheduling freedom)
     P.tan_ok = P.walsh_diag and mode == MODE_BWD
-    P.tan_mode = None  # "uncond": forward phase checked safe up front (emit_fwd_phases)
     P.slotf = prog.enc[pi]["slotf"]
     nv = 1 if mode == MODE_FWD else 2
     prefetch = stage_vectors(prog, pi, mode) > 0
@@ -1479,31 +1471,7 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
     def emit_fwd_phases(end):
         # forward phases carry psi only (the turnaround's lambda is formed after them)
         for k in range(end + 1):
-            rots = []
-            if TAN_ROT and TAN_FWD and P.walsh_diag:
-                for op in P.enc["ops"][k]:
-                    if int(op[0]) == S.OP_U1:
-                        grp = P.prog.groups[int(op[3])]
-                        if _group_const_matrix(grp, P.drop_phase) is None and is_rotation(grp):
-                            rots.append(int(op[5]))
-            if rots:
-                # one uniform branch per phase: every rotation safe (|c| >= TAN_TH) -> the phase
-                # runs all of them in tangent form, else the two-op form
-                cond = " && ".join(f"fabsf(s_mat[{m}]) >= {TAN_TH}f" for m in rots)
-                st0 = (P.rho_live, P.tan_count)
-                w(f"if ({cond}) {{")
-                P.tan_mode = "uncond"
-                _emit_ops(w, P, k, False, 1)
-                st1 = (P.rho_live, P.tan_count)
-                P.rho_live, P.tan_count = st0
-                P.tan_mode = None
-                w("} else {")
-                _emit_ops(w, P, k, False, 1)
-                w("}")
-                P.rho_live = P.rho_live or st1[0]
-                P.tan_count = max(P.tan_count, st1[1])
-            else:
-                _emit_ops(w, P, k, False, 1)
+            _emit_ops(w, P, k, False, 1)
             if k < end:
                 if rot is not None:
                     rot.exchange(w, P, k, k + 1, [0])
