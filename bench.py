@@ -199,7 +199,37 @@ class ClockSampler:
         self.proc = None
         self.t0 = self.t1 = None
 
+    def _nvml_loop(self):
+        """NVML poll every 2 ms (same counters as nvidia-smi, denser inside short regions)"""
+        import pynvml
+
+        bits = {"hw_slowdown": pynvml.nvmlClocksEventReasonHwSlowdown,
+                "hw_thermal_slowdown": pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                "sw_thermal_slowdown": pynvml.nvmlClocksEventReasonSwThermalSlowdown,
+                "sw_power_cap": pynvml.nvmlClocksEventReasonSwPowerCap}
+        hs = [pynvml.nvmlDeviceGetHandleByIndex(int(i)) for i in self.idx.split(",")]
+        while not self.stop:
+            now = time.time()
+            if self.w0 is not None and (self.w1 is None or now <= self.w1):
+                for h in hs:
+                    sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                    mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+                    r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.nv.append((sm, mx, sorted(k for k, b in bits.items() if r & b)))
+            time.sleep(0.002)
+
     def __enter__(self):
+        self.nv, self.stop, self.w0, self.w1 = [], False, None, None
+        try:
+            import threading
+
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.th = threading.Thread(target=self._nvml_loop, daemon=True)
+            self.th.start()
+        except Exception:
+            self.th = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", self.idx, f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
@@ -213,14 +243,19 @@ class ClockSampler:
         import datetime
 
         self.t0 = datetime.datetime.now()
+        self.w0 = time.time()
 
     def mark_end(self):
         import datetime
 
         self.t1 = datetime.datetime.now()
+        self.w1 = time.time()
         time.sleep(0.05)
 
     def __exit__(self, *a):
+        self.stop = True
+        if getattr(self, "th", None) is not None:
+            self.th.join(timeout=1)
         self.lines = []
         if self.proc is not None:
             self.proc.terminate()
@@ -244,6 +279,11 @@ class ClockSampler:
                 samples.append((ts, float(p[2]), float(p[3]), p[5:9]))
             except ValueError:
                 continue
+        nv = list(getattr(self, "nv", []))
+        if len(nv) >= 3:  # dense NVML samples inside the timed region
+            reasons = sorted({r for x in nv for r in x[2]})
+            return {"sm_mhz": statistics.median(x[0] for x in nv), "sm_max_mhz": max(x[1] for x in nv),
+                    "reasons": reasons, "samples": len(nv), "source": "nvml, 2 ms"}
         if not samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
         win = samples
@@ -259,7 +299,7 @@ class ClockSampler:
                 if v.lower() == "active":
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(x[1] for x in win), "sm_max_mhz": max(x[2] for x in win),
-                "reasons": sorted(reasons), "samples": len(win)}
+                "reasons": sorted(reasons), "samples": len(win), "source": "nvidia-smi, 20 ms"}
 
 
 def _pass_vectors(prog, mode, pidx, adjoint="recompute"):
