@@ -1149,6 +1149,10 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
             rot = _Rot(P, 1)
     est_regs = 2 * P.NR * nv + 40
     minb = max(1, min(4, 65536 // (P.NT * est_regs)))
+    if mode == MODE_FWD:
+        # forward kernels: an 80-register budget (measured: 256-thread tiles at 3 CTAs/SM beat 2,
+        # 128-thread tiles at 6 beat 4 -- occupancy wins over a few spills)
+        minb = max(1, min(8, 65536 // (P.NT * 80)))
     if os.environ.get("LSQ_MINB_FWD") and mode == MODE_FWD:
         minb = int(os.environ["LSQ_MINB_FWD"])
     matf = P.enc["matf"]
