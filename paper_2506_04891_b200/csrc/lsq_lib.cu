@@ -122,6 +122,77 @@ __global__ void k_reduce_z(const double* zpart, int cpr, int n, const double* wt
   }
 }
 
+#ifndef K_CONTRACT_1Q
+#define K_CONTRACT_1Q 1
+#endif
+// 2x2 complex helpers on register arrays (the one-qubit groups of k_contract)
+__device__ __forceinline__ void mul2(const cd* a, const cd* b, cd* o) {  // o = a b (o may alias)
+  const cd t0 = cadd(cmulx(a[0], b[0]), cmulx(a[1], b[2])), t1 = cadd(cmulx(a[0], b[1]), cmulx(a[1], b[3]));
+  const cd t2 = cadd(cmulx(a[2], b[0]), cmulx(a[3], b[2])), t3 = cadd(cmulx(a[2], b[1]), cmulx(a[3], b[3]));
+  o[0] = t0; o[1] = t1; o[2] = t2; o[3] = t3;
+}
+__device__ __forceinline__ void gate2(int code, const double* p, cd* o) {
+  cd m[16];
+  gate_matrix_dev(code, p, m);
+  o[0] = m[0]; o[1] = m[1]; o[2] = m[2]; o[3] = m[3];
+}
+__device__ __forceinline__ void dgate2(int code, const double* p, int k, cd* o) {
+  cd m[16];
+  gate_deriv_dev(code, p, k, m);
+  o[0] = m[0]; o[1] = m[1]; o[2] = m[2]; o[3] = m[3];
+}
+
+// one-qubit group of k_contract with register-resident 2x2 matrices (the generic path below
+// keeps 16-entry arrays in local memory for every group)
+__device__ void contract1q(const int* grp, const int* gates, const double* fvals, const double* theta,
+                           const double* xrow, const cd* M, int b, double* grows, int T, double* erows, int E) {
+  const int ngt = grp[GW_NG];
+  cd U[4] = {cd{1, 0}, cd{0, 0}, cd{0, 0}, cd{1, 0}};
+  for (int j = 0; j < ngt; ++j) {
+    const int* gw = gates + (grp[GW_G0] + j) * GATE_WORDS;
+    double p[3] = {0, 0, 0};
+    for (int k = 0; k < gw[7]; ++k) p[k] = gate_param(gw, k, fvals, theta, xrow);
+    cd G[4];
+    gate2(gw[0], p, G);
+    mul2(G, U, U);
+  }
+  const cd Ud[4] = {cd{U[0].r, -U[0].i}, cd{U[2].r, -U[2].i}, cd{U[1].r, -U[1].i}, cd{U[3].r, -U[3].i}};
+  cd A[4] = {cd{1, 0}, cd{0, 0}, cd{0, 0}, cd{1, 0}};
+  for (int j = 0; j < ngt; ++j) {
+    const int* gw = gates + (grp[GW_G0] + j) * GATE_WORDS;
+    double p[3] = {0, 0, 0};
+    for (int k = 0; k < gw[7]; ++k) p[k] = gate_param(gw, k, fvals, theta, xrow);
+    cd G[4], Bm[4] = {cd{1, 0}, cd{0, 0}, cd{0, 0}, cd{1, 0}};
+    gate2(gw[0], p, G);
+    for (int jj = j + 1; jj < ngt; ++jj) {
+      const int* gw2 = gates + (grp[GW_G0] + jj) * GATE_WORDS;
+      double p2[3] = {0, 0, 0};
+      for (int k = 0; k < gw2[7]; ++k) p2[k] = gate_param(gw2, k, fvals, theta, xrow);
+      cd G2[4];
+      gate2(gw2[0], p2, G2);
+      mul2(G2, Bm, Bm);
+    }
+    for (int k = 0; k < gw[7]; ++k) {
+      const int s = gw[2 + k];
+      if (s == -1) continue;
+      cd Wm[4];
+      dgate2(gw[0], p, k, Wm);
+      mul2(Wm, A, Wm);
+      mul2(Bm, Wm, Wm);
+      mul2(Wm, Ud, Wm);
+      double g = 0.0;
+      for (int e = 0; e < 4; ++e) g += Wm[e].r * M[e].r - Wm[e].i * M[e].i;
+      g *= 2.0;
+      if (s & ENC_FLAG) {
+        if (erows) erows[(size_t)b * E + (s & ~ENC_FLAG)] = g;
+      } else {
+        if (grows) grows[(size_t)b * T + s] = g;
+      }
+    }
+    mul2(G, A, A);
+  }
+}
+
 // per (row, group): grads of every parameter of every gate in the group,
 // g = 2 Re sum_ab W_ab M_ab,  W = (G_s..G_{j+1}) dG_j (G_{j-1}..G_1) U^dag
 __global__ void k_contract(const int* W, const double* fvals, const double* theta, const double* x,
@@ -151,6 +222,11 @@ __global__ void k_contract(const int* W, const double* fvals, const double* thet
       for (int e = 0; e < d; ++e) Mm[e * d + e] = cd{mrow[2 * e], mrow[2 * e + 1]};
     } else {
       for (int e = 0; e < d * d; ++e) Mm[e] = cd{mrow[2 * e], mrow[2 * e + 1]};
+    }
+    if (d == 2 && K_CONTRACT_1Q) {
+      const cd M2[4] = {Mm[0], Mm[1], Mm[2], Mm[3]};
+      contract1q(grp, gates, fvals, theta, xrow, M2, b, grows, T, erows, E);
+      continue;
     }
     cd U[16], Ud[16], A[16], Bm[16], G[16], dG[16], Wm[16];
     group_unitary(W, gid, fvals, theta, xrow, U);
