@@ -350,6 +350,12 @@ def run_ours(args, world, rank, local):
 
         prow = max(1, min(b, (2 << 30) // (8 << wl.n)))
         M_best, st = choose_tile_bits(wl.circuit, prow, Objective.FORWARD_BACKWARD, device=dev)
+        if world > 1:  # one tiling for every rank (rank 0's measurement)
+            import torch.distributed as dist
+
+            mt = torch.tensor([M_best], device=dev, dtype=torch.int64)
+            dist.broadcast(mt, src=0)
+            M_best = int(mt.item())
         tile_choice = {"rows": prow, "ms": {str(m): round(v.mean_seconds * 1e3, 3) for m, v in st.items()}}
         plan = plan_for_tile_bits(wl.circuit, b, M_best)
         args.M = M_best
