@@ -313,31 +313,35 @@ def expectation_z(psi: np.ndarray, n: int) -> np.ndarray:
 # ----------------------------------------------------------------------------- forward
 
 
-def _layer_mats(circuit, i, sl, trainable, encoding):
+def _layer_mats(circuit, i, sl, trainable, encoding, dtype=complex):
     layer = circuit.layers[i]
     name = _name(layer)
     pos = positions(layer, circuit.n)
     par = layer_params(circuit, i, sl, trainable, encoding)
     if par is None:
-        m = gate_matrix(name)
+        m = gate_matrix(name).astype(dtype)
         return [m] * len(pos)
     if par.ndim == 2:
-        return [gate_matrix(name, par[j]) for j in range(len(pos))]
-    return [gate_matrix(name, par[:, j]) for j in range(len(pos))]
+        return [gate_matrix(name, par[j]).astype(dtype) for j in range(len(pos))]
+    return [gate_matrix(name, par[:, j]).astype(dtype) for j in range(len(pos))]
 
 
-def apply_circuit(circuit, trainable=None, encoding=None, state=None, batch=1):
+def apply_circuit(circuit, trainable=None, encoding=None, state=None, batch=1, dtype=complex):
     """Forward pass on a copy of `state` (default |0..0>), one pass per gate position
-    (the reference's einsum kernel, kernels.py:611-622)."""
+    (the reference's einsum kernel, kernels.py:611-622).
+
+    `dtype=np.complex64` runs the same algorithm with complex64 states, matrices and einsum
+    accumulation: a precision model of a single-precision engine (test-only, used to show
+    which deviations are the complex64 rounding floor rather than a kernel defect)."""
     n = circuit.n
     if state is None:
-        psi = np.zeros((batch, 1 << n), dtype=complex)
+        psi = np.zeros((batch, 1 << n), dtype=dtype)
         psi[:, 0] = 1.0
     else:
-        psi = np.array(state, dtype=complex, copy=True)
+        psi = np.array(state, dtype=dtype, copy=True)
     sl, _, _ = slots(circuit)
     for i, layer in enumerate(circuit.layers):
-        mats = _layer_mats(circuit, i, sl, trainable, encoding)
+        mats = _layer_mats(circuit, i, sl, trainable, encoding, dtype)
         for ws, m in zip(positions(layer, n), mats):
             apply_gate(psi, m, [n - 1 - w for w in ws])
     return psi
@@ -368,15 +372,17 @@ def _disjoint(pos):
     return True
 
 
-def backward_sweep(circuit, trainable, encoding, final, weights=None, need_encoding=True):
+def backward_sweep(circuit, trainable, encoding, final, weights=None, need_encoding=True,
+                   dtype=complex):
     """Adjoint reverse sweep (reference grad.py:169-204) with the weighted observable.
 
     Returns (value (B,), grads (B,T), encoding_grads (B,E)).
     """
     n = circuit.n
     sl, T, E = slots(circuit)
-    psi = np.array(final, dtype=complex, copy=True)
-    d = z_diag(n, weights)
+    psi = np.array(final, dtype=dtype, copy=True)
+    real = np.float32 if np.dtype(dtype) == np.complex64 else float
+    d = z_diag(n, weights).astype(real)
     lam = psi * d[None, :]
     batch = psi.shape[0]
     grads = np.zeros((batch, T))
@@ -388,7 +394,7 @@ def backward_sweep(circuit, trainable, encoding, final, weights=None, need_encod
         layer = circuit.layers[i]
         name = _name(layer)
         s = sl[i]
-        mats = _layer_mats(circuit, i, sl, trainable, encoding)
+        mats = _layer_mats(circuit, i, sl, trainable, encoding, dtype)
         pos = positions(layer, n)
         need = s is not None and s[0] in ("trainable", "encoding")
         if not need:
@@ -407,7 +413,7 @@ def backward_sweep(circuit, trainable, encoding, final, weights=None, need_encod
                 pj = par[j] if par.ndim == 2 else par[:, j]
                 m = coupling(lam, psi, bits[j])
                 for kk in range(k):
-                    v = dagger(mats[j]) @ gate_derivative(name, pj, kk)
+                    v = dagger(mats[j]) @ gate_derivative(name, pj, kk).astype(dtype)
                     out[:, j, kk] = _contract(v, m)
         else:
             # descending rule: peel gate by gate
@@ -416,7 +422,7 @@ def backward_sweep(circuit, trainable, encoding, final, weights=None, need_encod
                 apply_gate(psi, dagger(mats[j]), bits[j])
                 m = coupling(lam, psi, bits[j])
                 for kk in range(k):
-                    dv = gate_derivative(name, pj, kk)
+                    dv = gate_derivative(name, pj, kk).astype(dtype)
                     out[:, j, kk] = _contract(dv, m)
                 apply_gate(lam, dagger(mats[j]), bits[j])
         flat = out.reshape(batch, -1)
@@ -428,10 +434,11 @@ def backward_sweep(circuit, trainable, encoding, final, weights=None, need_encod
     return value, grads, egrads
 
 
-def gradient(circuit, trainable=None, encoding=None, batch=1, weights=None, need_encoding=True):
+def gradient(circuit, trainable=None, encoding=None, batch=1, weights=None, need_encoding=True,
+             dtype=complex):
     """Forward from |0..0> then the adjoint sweep (reference grad.py:207-218).
 
     Returns dict(value (B,), zq (B,n), grads (B,T), encoding_grads (B,E))."""
-    final = apply_circuit(circuit, trainable, encoding, batch=batch)
-    value, g, eg = backward_sweep(circuit, trainable, encoding, final, weights, need_encoding)
+    final = apply_circuit(circuit, trainable, encoding, batch=batch, dtype=dtype)
+    value, g, eg = backward_sweep(circuit, trainable, encoding, final, weights, need_encoding, dtype)
     return {"value": value, "zq": expectation_z(final, circuit.n), "grads": g, "encoding_grads": eg}

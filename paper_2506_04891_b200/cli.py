@@ -90,6 +90,14 @@ def _build_parser():
     s.add_argument("--warmup", type=int, default=3)
     s.add_argument("--seed", type=int, default=0)
     s.add_argument("--out", required=True)
+    s = sub.add_parser("compile", help="compile a circuit into a program artifact for lsq_program_load")
+    g = s.add_mutually_exclusive_group(required=True)
+    g.add_argument("--circuit", help="reference circuit JSON file")
+    g.add_argument("--config", type=int, choices=[1, 2, 3, 4, 5], help="a BASELINE config circuit")
+    s.add_argument("--plan", default=None, help="plan JSON (tile exponent, isolated layers)")
+    s.add_argument("--gradient", action="store_true",
+                   help="gradient program (synthesized |0..0> prefix, folded observable)")
+    s.add_argument("--out", required=True)
     return p
 
 
@@ -135,7 +143,32 @@ def _cmd_plan(args) -> int:
     return 0
 
 
-_COMMANDS = {"run": _cmd_run, "grad": _cmd_grad, "plan": _cmd_plan}
+def _cmd_compile(args) -> int:
+    """Host-only (no GPU): circuit -> schedule -> generated kernels -> one artifact file."""
+    from . import artifact
+    from .planner import KernelKind, load_plan, tiling_of
+    from .schedule import DEFAULT_M, DEFAULT_R_SPECIALISED, compile_circuit, default_r
+
+    if args.circuit is not None:
+        circuit = load_circuit(args.circuit)
+    else:
+        from .configs import build_config_circuit
+
+        circuit = build_config_circuit(args.config)
+    plan = load_plan(args.plan) if args.plan is not None else None
+    M, R = tiling_of(plan, circuit)
+    if R is None:
+        m = min(circuit.n, M if M is not None else DEFAULT_M)
+        R = DEFAULT_R_SPECIALISED if m >= 9 else default_r(m)
+    isolate = [] if plan is None else [i for i, k in enumerate(plan.assignments) if k is KernelKind.ISOLATED]
+    prog = compile_circuit(circuit, M=M, R=R, isolate=isolate, prefix=args.gradient, fold=args.gradient,
+                           split=True)
+    size = artifact.write(prog, args.out)
+    print(f"wrote {args.out}: n={circuit.n}, {len(prog.passes)} passes, {size} bytes")
+    return 0
+
+
+_COMMANDS = {"run": _cmd_run, "grad": _cmd_grad, "plan": _cmd_plan, "compile": _cmd_compile}
 
 
 def main(argv=None) -> int:

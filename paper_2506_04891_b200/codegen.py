@@ -1,9 +1,9 @@
 """Per-circuit CUDA code generation: one straight-line sm_100a kernel per (pass, mode).
 
-The generic pass kernel (`csrc/lsq_pass.cuh`) interprets the op words at run time; its
-dispatch over runtime register indices makes the compiler copy the whole 64-register
-amplitude tile at every op (ncu: 54% of executed instructions were MOVs, profiles/). Here
-the same schedule is emitted as straight-line code compiled by NVRTC for sm_100a at program
+A kernel that interprets the op words at run time (round 1's generic kernel, since removed)
+dispatches over run-time register indices, which makes the compiler copy the whole
+64-register amplitude tile at every op (ncu: 54% of executed instructions were MOVs). Here
+the schedule is emitted as straight-line code compiled by NVRTC for sm_100a at program
 creation, so that
 
 * register-bit indices, tile layouts and global/shared offsets are compile-time constants;
@@ -13,8 +13,9 @@ creation, so that
   structural zeros cost nothing;
 * a diagonal run accumulates fixed-point phases with compile-time index selection.
 
-The emitted kernels keep the generic kernel's contract (PassArgs, modes, flags, partial
-buffers), so the C ABI drivers and the emulator semantics are unchanged.
+The emitted kernels share one launch contract (PassArgs, modes, flags, partial buffers,
+csrc/lsq_prims.cuh) with the C-ABI drivers; the CPU emulator (tests/emulator.py) interprets
+the same program words.
 """
 
 from __future__ import annotations

@@ -104,6 +104,9 @@ def build_config_circuit(cfg: int, n: int | None = None, zz_pattern: str = "chai
     return Circuit(n, layers)
 
 
+# (encoding/head layers, layers per repeated block, blocks) of each config circuit
+BLOCK_LAYOUT = {1: (1, 3, 2), 2: (1, 3, 4), 3: (1, 4, 3), 4: (2, 5, 4), 5: (1, 5, 6)}
+
 CONFIG_SHAPES = {1: (8, 64), 2: (16, 512), 3: (20, 128), 4: (22, 256), 5: (24, 1024)}
 CONFIG_NAMES = {
     1: "cfg1_n8_b64_rx_rz_cnotring",

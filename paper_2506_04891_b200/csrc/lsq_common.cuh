@@ -12,6 +12,13 @@ namespace lsq {
 
 // ---- program words (schedule.py) -------------------------------------------------------
 constexpr int MAGIC = 0x4C535131;
+// pass modes and flags (the specialised kernels' PassArgs contract, lsq_prims.cuh PMODE_/PF_)
+constexpr int MODE_FWD = 0, MODE_TURN = 1, MODE_BWD = 2;
+constexpr int F_SYNTH = 1,      // input psi is |0..0> (not read)
+    F_STORE_PSI = 2,            // write psi at the end of the pass
+    F_STORE_LAM = 4,            // write lambda at the end of the pass
+    F_ZPART = 8,                // forward: accumulate <Z_q> partials of the output
+    F_NOFWD = 16;               // turnaround on a given final state: skip the forward ops
 constexpr int HDR_WORDS = 32, GATE_WORDS = 8, GROUP_WORDS = 16, PASS_WORDS = 24,
               PHASE_WORDS = 24, OP_WORDS = 8, SUB_WORDS = 8, PGROUP_WORDS = 4;
 constexpr int SEC_GATES = 0, SEC_GROUPS = 1, SEC_PASSES = 2, SEC_PHASES = 3, SEC_OPS = 4,

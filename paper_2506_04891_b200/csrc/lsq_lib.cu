@@ -22,14 +22,35 @@
 
 #include "../../include/layersim_cuda.h"
 #include "lsq_common.cuh"
-#include "lsq_pass.cuh"
-#include "lsq_kernels.h"
+#include "lsq_prims.cuh"
 
 using namespace lsq;
 
 namespace {
 
 thread_local std::string g_err;
+
+// Per-call bookkeeping lives with the CALLING HOST THREAD, never in the program: a program is
+// immutable once lsq_program_jit has attached its kernels, so any number of host threads and
+// streams can run it concurrently (each thread sees the launch count / pass timings of its
+// own last call).
+struct CallState {
+  bool profiling = false;
+  std::vector<cudaEvent_t> ev;  // pool: 2 events per profiled pass launch
+  int ev_used = 0;
+  std::vector<int> kinds;
+  int launches = 0;
+  ~CallState() {
+    for (auto e : ev) cudaEventDestroy(e);
+  }
+};
+thread_local CallState g_call;
+
+void begin_call() {
+  g_call.ev_used = 0;
+  g_call.kinds.clear();
+  g_call.launches = 0;
+}
 
 int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -294,25 +315,6 @@ __global__ void k_sum_rows(const double* grows, int batch, int T, double* out) {
   }
 }
 
-// ---- pass kernel table (instantiated in lsq_inst.cu, one TU each) -------------------------
-using PassFn = void (*)(PassArgs);
-
-struct KEntry {
-  PassFn fn;
-  int M, R, NV, NT;
-};
-
-KEntry kernel_for(int M, int NV) {
-#define LSQ_TRY(m, nv)                                           \
-  if (M == m && NV == nv) {                                      \
-    KernelEntry e = lsq_kernel_entry_##m##_##nv();               \
-    return KEntry{(PassFn)e.fn, e.M, e.R, e.NV, e.NT};           \
-  }
-  LSQ_FOR_EACH_KERNEL(LSQ_TRY)
-#undef LSQ_TRY
-  return KEntry{nullptr, M, 0, NV, 0};
-}
-
 int pow2floor(int64_t v) {
   int r = 1;
   while ((int64_t)r * 2 <= v) r *= 2;
@@ -323,7 +325,6 @@ int pow2floor(int64_t v) {
 
 struct PassInfo {
   int M, R, nph, slotf, matf, nops, nsubs, first_slot;
-  KEntry k1, k2;
 };
 
 struct JitKernel {
@@ -334,7 +335,7 @@ struct JitKernel {
 };
 
 struct lsq_program {
-  std::vector<JitKernel> jit;  // [pass * 3 + mode], fn == nullptr -> generic kernel
+  std::vector<JitKernel> jit;  // [pass * 3 + mode]: the specialised kernel of each pass and mode
   std::vector<cudaLibrary_t> jit_libs;
   int n, T, E, npasses, ngroups, slot_total, nperrow, prefix = 0, obs = 0;
   int* d_words = nullptr;
@@ -342,11 +343,6 @@ struct lsq_program {
   std::vector<int> words;
   std::vector<PassInfo> passes;
   int sm_count = 148;
-  bool profiling = false;
-  std::vector<cudaEvent_t> ev;  // pool: 2 events per profiled pass launch
-  int ev_used = 0;
-  std::vector<int> kinds;
-  int launches = 0;  // kernels launched by the last call
 };
 
 namespace {
@@ -362,21 +358,6 @@ size_t smem_bytes(const lsq_program* P, const PassInfo& pi, int NV) {
   b += sizeof(float) * NW * 32;  // per-warp <Z> / reduction scratch (n + 1 <= 32, M + 1 <= 32)
   b += sizeof(float) * NW * 8;   // specialised kernels: coupling half-block padding per warp
   return (b + 15) & ~(size_t)15;
-}
-
-// The dynamic shared-memory opt-in is a per-kernel-function attribute shared by every
-// program in the process: only ever raise it.
-std::mutex g_smem_mu;
-std::map<const void*, size_t> g_smem_max;
-
-int ensure_smem(PassFn fn, size_t bytes) {
-  std::lock_guard<std::mutex> lock(g_smem_mu);
-  size_t& cur = g_smem_max[(const void*)fn];
-  if (bytes <= cur) return LSQ_OK;
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  if (e != cudaSuccess) return fail(LSQ_ECUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
-  cur = bytes;
-  return LSQ_OK;
 }
 
 struct Geometry {
@@ -475,19 +456,15 @@ WS carve(const lsq_program* P, int batch, void* base) {
   return w;
 }
 
-int launch_pass(lsq_program* P, int pi_idx, int mode, int flags, int batch, const double* theta,
+int launch_pass(const lsq_program* P, int pi_idx, int mode, int flags, int batch, const double* theta,
                 const double* x, int x_stride, const double* w, const float2* psi_in, float2* psi_out,
                 float2* lam, const WS& ws, cudaStream_t st) {
   const PassInfo& pi = P->passes[pi_idx];
-  const int NV = mode == MODE_FWD ? 1 : 2;
-  const KEntry& k = NV == 1 ? pi.k1 : pi.k2;
-  const bool have_jit = !P->jit.empty() && P->jit[pi_idx * 3 + mode].fn;
-  if ((P->prefix || P->obs) && !have_jit)
-    return fail(LSQ_EPLAN, "programs with a synthesized prefix or a folded observable need the specialised kernels");
-  if (!k.fn && !have_jit)
-    return fail(LSQ_EPLAN, "no kernel for pass " + std::to_string(pi_idx) + " (M=" + std::to_string(pi.M) +
-                               ", R=" + std::to_string(pi.R) + "): attach the specialised kernels");
-  Geometry g = geometry(P, pi_idx, have_jit ? mode : -1, batch);
+  const JitKernel* jk = P->jit.empty() ? nullptr : &P->jit[pi_idx * 3 + mode];
+  if (!jk || !jk->fn)
+    return fail(LSQ_EPLAN, "no kernel for pass " + std::to_string(pi_idx) + " mode " + std::to_string(mode) +
+                               ": attach the program's specialised kernels first (lsq_program_jit)");
+  Geometry g = geometry(P, pi_idx, mode, batch);
   PassArgs A{};
   A.prog = P->d_words;
   A.fvals = P->d_fvals;
@@ -510,65 +487,58 @@ int launch_pass(lsq_program* P, int pi_idx, int mode, int flags, int batch, cons
   A.wts = w;
   A.part = ws.part;
   A.zpart = ws.zpart;
-  const JitKernel* jk = nullptr;
-  if (!P->jit.empty() && P->jit[pi_idx * 3 + mode].fn) jk = &P->jit[pi_idx * 3 + mode];
-  const size_t sm = jk ? jk->smem_set : smem_bytes(P, pi, NV);
-  if (P->profiling) {
-    while ((int)P->ev.size() < 2 * (P->ev_used + 1)) {
+  CallState& C = g_call;
+  if (C.profiling) {
+    while ((int)C.ev.size() < 2 * (C.ev_used + 1)) {
       cudaEvent_t e;
       CUDA_TRY(cudaEventCreate(&e));
-      P->ev.push_back(e);
+      C.ev.push_back(e);
     }
-    CUDA_TRY(cudaEventRecord(P->ev[2 * P->ev_used], st));
+    CUDA_TRY(cudaEventRecord(C.ev[2 * C.ev_used], st));
   }
-  if (jk) {
-    void* args[] = {&A};
-    CUDA_TRY(cudaLaunchKernel(jk->fn, dim3((unsigned)((int64_t)batch * g.cpr)), dim3(jk->NT), args, sm, st));
-  } else {
-    k.fn<<<(unsigned)((int64_t)batch * g.cpr), k.NT, sm, st>>>(A);
-    CUDA_TRY(cudaGetLastError());
+  void* args[] = {&A};
+  CUDA_TRY(cudaLaunchKernel(jk->fn, dim3((unsigned)((int64_t)batch * g.cpr)), dim3(jk->NT), args, jk->smem_set, st));
+  C.launches++;
+  if (C.profiling) {
+    CUDA_TRY(cudaEventRecord(C.ev[2 * C.ev_used + 1], st));
+    C.kinds.push_back(mode * 1000 + pi_idx);
+    C.ev_used++;
   }
-  P->launches++;
-  if (P->profiling) {
-    CUDA_TRY(cudaEventRecord(P->ev[2 * P->ev_used + 1], st));
-    P->kinds.push_back(mode * 1000 + pi_idx);
-    P->ev_used++;
-  }
-  if (pi.slotf > 0 && NV == 2) {
+  if (pi.slotf > 0 && mode != MODE_FWD) {
     const int64_t tot = (int64_t)batch * pi.slotf;
     const int blocks = (int)std::min<int64_t>((tot + 255) / 256, 4096);
     k_reduce_part<<<blocks, 256, 0, st>>>(ws.part, g.cpr, pi.slotf, ws.macc, P->slot_total, pi.first_slot, batch);
     CUDA_TRY(cudaGetLastError());
-    P->launches++;
+    C.launches++;
   }
   return LSQ_OK;
 }
 
-int finish_grads(lsq_program* P, int batch, const double* theta, const double* x, int x_stride,
+int finish_grads(const lsq_program* P, int batch, const double* theta, const double* x, int x_stride,
                  const WS& ws, double* grad_rows, double* grad_sum, double* egrad_rows, cudaStream_t st) {
   double* grows = grad_rows ? grad_rows : ws.grows;
   double* erows = egrad_rows ? egrad_rows : (P->E ? ws.erows : nullptr);
   if (P->T) {
     const int64_t t = (int64_t)batch * P->T;
     k_zero<<<(int)std::min<int64_t>((t + 255) / 256, 4096), 256, 0, st>>>(grows, t);
-    P->launches++;
+    g_call.launches++;
   }
   if (erows) {
     const int64_t t = (int64_t)batch * P->E;
     k_zero<<<(int)std::min<int64_t>((t + 255) / 256, 4096), 256, 0, st>>>(erows, t);
-    P->launches++;
+    g_call.launches++;
   }
   {
     const int64_t tot = (int64_t)batch * P->ngroups;
     const int blocks = (int)std::min<int64_t>((tot + 127) / 128, 8192);
     k_contract<<<std::max(blocks, 1), 128, 0, st>>>(P->d_words, P->d_fvals, theta, x, x_stride, ws.macc,
                                                    P->slot_total, batch, grows, P->T, erows, P->E);
-    P->launches++;
+    g_call.launches++;
     CUDA_TRY(cudaGetLastError());
   }
   if (grad_sum && P->T) {
     k_sum_rows<<<std::min(P->T, 4096), 256, 0, st>>>(grows, batch, P->T, grad_sum);
-    P->launches++;
+    g_call.launches++;
     CUDA_TRY(cudaGetLastError());
   }
   return LSQ_OK;
@@ -632,22 +602,7 @@ int lsq_program_create(const int32_t* words, int64_t n_words, const double* fval
     pi.nops = pw[PW_OPN];
     pi.nsubs = pw[PW_SUBN];
     pi.first_slot = pw[PW_FIRSTSLOT];
-    pi.k1 = kernel_for(pi.M, 1);
-    pi.k2 = kernel_for(pi.M, 2);
-    // the generic (interpreting) kernels exist for R = r_of(M) only; other register tilings
-    // run exclusively on the per-program specialised kernels (lsq_program_jit)
-    if (pi.k1.R != pi.R) pi.k1.fn = nullptr;
-    if (pi.k2.R != pi.R) pi.k2.fn = nullptr;
     P->passes.push_back(pi);
-    for (int NV = 1; NV <= 2; ++NV) {
-      const KEntry& k = NV == 1 ? pi.k1 : pi.k2;
-      if (!k.fn) continue;
-      int rc = ensure_smem(k.fn, smem_bytes(P, pi, NV));
-      if (rc) {
-        delete P;
-        return rc;
-      }
-    }
   }
   cudaError_t e1 = cudaMalloc(&P->d_words, sizeof(int) * n_words);
   cudaError_t e2 = cudaMalloc(&P->d_fvals, sizeof(double) * std::max<int64_t>(n_fvals, 1));
@@ -829,10 +784,66 @@ int lsq_program_jit(lsq_program* P, int nk, const char* const* sources, const in
   return LSQ_OK;
 }
 
+int lsq_program_load(const char* path, const char* cache_dir, lsq_program** out) {
+  if (!path || !out) return fail(LSQ_EINVAL, "null argument");
+  std::string blob;
+  if (!read_file(path, blob)) return fail(LSQ_EINVAL, std::string("cannot read program artifact ") + path);
+  size_t off = 0;
+  auto take = [&](void* dst, size_t n) {
+    if (off + n > blob.size()) return false;
+    memcpy(dst, blob.data() + off, n);
+    off += n;
+    return true;
+  };
+  char magic[4];
+  uint32_t version = 0;
+  int64_t nw = 0, nf = 0;
+  int32_t nk = 0;
+  if (!take(magic, 4) || memcmp(magic, "LSQP", 4) != 0) return fail(LSQ_EINVAL, "not a program artifact (magic)");
+  if (!take(&version, 4)) return fail(LSQ_EINVAL, "truncated program artifact");
+  if (version != 1) return fail(LSQ_EPLAN, "program artifact version " + std::to_string(version) + " != 1");
+  if (!take(&nw, 8) || !take(&nf, 8) || !take(&nk, 4) || nw < HDR_WORDS || nf < 0 || nk < 0 ||
+      (size_t)nw > blob.size() / 4 || (size_t)nf > blob.size() / 8)
+    return fail(LSQ_EINVAL, "corrupt program artifact header");
+  std::vector<int32_t> words((size_t)nw);
+  std::vector<double> fvals((size_t)std::max<int64_t>(nf, 1));
+  if (!take(words.data(), 4 * (size_t)nw) || !take(fvals.data(), 8 * (size_t)nf))
+    return fail(LSQ_EINVAL, "truncated program artifact (words)");
+  std::vector<std::string> srcs((size_t)nk), names((size_t)nk);
+  std::vector<int> pidx((size_t)nk), modes((size_t)nk), stages((size_t)nk);
+  for (int i = 0; i < nk; ++i) {
+    int32_t nl = 0;
+    int64_t sl = 0;
+    if (!take(&pidx[i], 4) || !take(&modes[i], 4) || !take(&stages[i], 4) || !take(&nl, 4) || nl < 1 ||
+        (size_t)nl > blob.size() - off)
+      return fail(LSQ_EINVAL, "corrupt program artifact (kernel header)");
+    names[i].resize((size_t)nl);
+    if (!take(&names[i][0], (size_t)nl) || !take(&sl, 8) || sl < 1 || (size_t)sl > blob.size() - off)
+      return fail(LSQ_EINVAL, "corrupt program artifact (kernel source)");
+    srcs[i].resize((size_t)sl);
+    take(&srcs[i][0], (size_t)sl);
+  }
+  if (off != blob.size()) return fail(LSQ_EINVAL, "trailing bytes in program artifact");
+  lsq_program* P = nullptr;
+  int rc = lsq_program_create(words.data(), nw, fvals.data(), nf, &P);
+  if (rc) return rc;
+  std::vector<const char*> sp((size_t)nk), np((size_t)nk);
+  for (int i = 0; i < nk; ++i) {
+    sp[i] = srcs[i].c_str();
+    np[i] = names[i].c_str();
+  }
+  rc = lsq_program_jit(P, nk, sp.data(), pidx.data(), modes.data(), stages.data(), np.data(), cache_dir, 0);
+  if (rc) {
+    lsq_program_destroy(P);
+    return rc;
+  }
+  *out = P;
+  return LSQ_OK;
+}
+
 void lsq_program_destroy(lsq_program* P) {
   if (!P) return;
   for (auto l : P->jit_libs) cudaLibraryUnload(l);
-  for (auto e : P->ev) cudaEventDestroy(e);
   cudaFree(P->d_words);
   cudaFree(P->d_fvals);
   delete P;
@@ -850,26 +861,27 @@ int64_t lsq_workspace_bytes(const lsq_program* P, int batch) {
   return (int64_t)carve(P, batch, nullptr).bytes;
 }
 
-int lsq_set_profiling(lsq_program* P, int on) {
+int lsq_set_profiling(const lsq_program* P, int on) {
   if (!P) return fail(LSQ_EINVAL, "null program");
-  P->profiling = on != 0;
+  g_call.profiling = on != 0;
   return LSQ_OK;
 }
 
 int lsq_last_pass_times(const lsq_program* P, float* ms, int cap, int* kinds) {
   if (!P) return -1;
-  const int n = P->ev_used;
-  if (n > 0 && cudaEventSynchronize(P->ev[2 * n - 1]) != cudaSuccess) return -1;
+  const CallState& C = g_call;
+  const int n = C.ev_used;
+  if (n > 0 && cudaEventSynchronize(C.ev[2 * n - 1]) != cudaSuccess) return -1;
   for (int i = 0; i < n && i < cap; ++i) {
     float t = 0.f;
-    cudaEventElapsedTime(&t, P->ev[2 * i], P->ev[2 * i + 1]);
+    cudaEventElapsedTime(&t, C.ev[2 * i], C.ev[2 * i + 1]);
     if (ms) ms[i] = t;
-    if (kinds) kinds[i] = P->kinds[i];
+    if (kinds) kinds[i] = C.kinds[i];
   }
   return n;
 }
 
-int lsq_last_launch_count(const lsq_program* P) { return P ? P->launches : -1; }
+int lsq_last_launch_count(const lsq_program* P) { return P ? g_call.launches : -1; }
 
 int lsq_jit_compiler(char* buf, int buflen) {
   const Nvrtc& R = nvrtc();
@@ -882,26 +894,24 @@ int lsq_jit_compiler(char* buf, int buflen) {
 int lsq_forward(const lsq_program* Pc, int batch, const double* theta, const double* x, int x_stride,
                 const double* w, const void* psi_in, void* psi_out, double* zq, double* value,
                 void* workspace, void* stream) {
-  auto* P = const_cast<lsq_program*>(Pc);
+  const lsq_program* P = Pc;
   if (!P || batch < 1 || !psi_out || !workspace) return fail(LSQ_EINVAL, "null argument");
   if (P->T && !theta) return fail(LSQ_EINVAL, "circuit has trainable parameters but none given");
   if (P->E && !x) return fail(LSQ_EINVAL, "circuit has encoding parameters but none given");
   cudaStream_t st = (cudaStream_t)stream;
   WS ws = carve(P, batch, workspace);
-  P->ev_used = 0;
-  P->kinds.clear();
-  P->launches = 0;
+  begin_call();
   k_group_table<<<std::max(1, (P->ngroups + 127) / 128), 128, 0, st>>>(P->d_words, P->d_fvals, theta, ws.gmats);
-  P->launches++;
+  g_call.launches++;
   if (P->nperrow && x) {
     const int64_t tot = (int64_t)batch * P->ngroups;
     k_row_table<<<(int)std::min<int64_t>((tot + 127) / 128, 8192), 128, 0, st>>>(P->d_words, P->d_fvals, theta, x, x_stride, batch, ws.rowtab);
-    P->launches++;
+    g_call.launches++;
   }
   if (P->prefix) {
     const int64_t tot = (int64_t)batch * P->n;
     k_prefix_table<<<(int)std::min<int64_t>((tot + 127) / 128, 8192), 128, 0, st>>>(P->d_words, P->d_fvals, theta, x, x_stride, batch, ws.ptab);
-    P->launches++;
+    g_call.launches++;
   }
   CUDA_TRY(cudaGetLastError());
   const float2* src = (const float2*)psi_in;
@@ -919,7 +929,7 @@ int lsq_forward(const lsq_program* Pc, int batch, const double* theta, const dou
   if (want_z) {
     Geometry g = geometry(P, P->npasses - 1, MODE_FWD, batch);
     k_reduce_z<<<(batch + 127) / 128, 128, 0, st>>>(ws.zpart, g.cpr, P->n, w, zq, value, batch);
-    P->launches++;
+    g_call.launches++;
     CUDA_TRY(cudaGetLastError());
   }
   return LSQ_OK;
@@ -936,34 +946,32 @@ int lsq_fwd_bwd_ckpt(const lsq_program* Pc, int batch, const double* theta, cons
                      const double* w, void* psi_v, void* lam_v, void* ckpt_v, double* zq, double* value,
                      double* grad_rows, double* grad_sum, double* egrad_rows, void* workspace,
                      void* stream) {
-  auto* P = const_cast<lsq_program*>(Pc);
+  const lsq_program* P = Pc;
   if (!P || batch < 1 || !psi_v || !lam_v || !workspace) return fail(LSQ_EINVAL, "null argument");
   if (P->T && !theta) return fail(LSQ_EINVAL, "circuit has trainable parameters but none given");
   if (P->E && !x) return fail(LSQ_EINVAL, "circuit has encoding parameters but none given");
   if (P->npasses == 0) return fail(LSQ_EPLAN, "empty program");
   cudaStream_t st = (cudaStream_t)stream;
   WS ws = carve(P, batch, workspace);
-  P->ev_used = 0;
-  P->kinds.clear();
-  P->launches = 0;
+  begin_call();
   float2* psi = (float2*)psi_v;
   float2* lam = (float2*)lam_v;
   k_group_table<<<std::max(1, (P->ngroups + 127) / 128), 128, 0, st>>>(P->d_words, P->d_fvals, theta, ws.gmats);
-  P->launches++;
+  g_call.launches++;
   if (P->nperrow && x) {
     const int64_t tot = (int64_t)batch * P->ngroups;
     k_row_table<<<(int)std::min<int64_t>((tot + 127) / 128, 8192), 128, 0, st>>>(P->d_words, P->d_fvals, theta, x, x_stride, batch, ws.rowtab);
-    P->launches++;
+    g_call.launches++;
   }
   if (P->prefix) {
     const int64_t tot = (int64_t)batch * P->n;
     k_prefix_table<<<(int)std::min<int64_t>((tot + 127) / 128, 8192), 128, 0, st>>>(P->d_words, P->d_fvals, theta, x, x_stride, batch, ws.ptab);
-    P->launches++;
+    g_call.launches++;
   }
   CUDA_TRY(cudaGetLastError());
   const int64_t mtot = (int64_t)batch * std::max(P->slot_total, 1);
   k_zero<<<(int)std::min<int64_t>((mtot + 255) / 256, 4096), 256, 0, st>>>(ws.macc, mtot);
-  P->launches++;
+  g_call.launches++;
   const int L = P->npasses;
   // checkpoint mode: pass i writes its output to ckpt[i] (i < L-1); the adjoint reads psi from
   // the checkpoints and writes lambda only. Otherwise psi is un-computed in place.
@@ -983,7 +991,7 @@ int lsq_fwd_bwd_ckpt(const lsq_program* Pc, int batch, const double* theta, cons
     if (rc) return rc;
     Geometry g = geometry(P, L - 1, MODE_TURN, batch);
     k_reduce_z<<<(batch + 127) / 128, 128, 0, st>>>(ws.zpart, g.cpr, P->n, w, zq, value, batch);
-    P->launches++;
+    g_call.launches++;
     CUDA_TRY(cudaGetLastError());
   }
   for (int i = L - 2; i >= 0; --i) {
@@ -999,7 +1007,7 @@ int lsq_bwd_from_state(const lsq_program* Pc, int batch, const double* theta, co
                        int x_stride, const double* w, const void* final_state, void* psi_v, void* lam_v,
                        double* zq, double* value, double* grad_rows, double* grad_sum,
                        double* egrad_rows, void* workspace, void* stream) {
-  auto* P = const_cast<lsq_program*>(Pc);
+  const lsq_program* P = Pc;
   if (!P || batch < 1 || !final_state || !psi_v || !lam_v || !workspace)
     return fail(LSQ_EINVAL, "null argument");
   if (P->T && !theta) return fail(LSQ_EINVAL, "circuit has trainable parameters but none given");
@@ -1007,27 +1015,25 @@ int lsq_bwd_from_state(const lsq_program* Pc, int batch, const double* theta, co
   if (P->npasses == 0) return fail(LSQ_EPLAN, "empty program");
   cudaStream_t st = (cudaStream_t)stream;
   WS ws = carve(P, batch, workspace);
-  P->ev_used = 0;
-  P->kinds.clear();
-  P->launches = 0;
+  begin_call();
   float2* psi = (float2*)psi_v;
   float2* lam = (float2*)lam_v;
   k_group_table<<<std::max(1, (P->ngroups + 127) / 128), 128, 0, st>>>(P->d_words, P->d_fvals, theta, ws.gmats);
-  P->launches++;
+  g_call.launches++;
   if (P->nperrow && x) {
     const int64_t tot = (int64_t)batch * P->ngroups;
     k_row_table<<<(int)std::min<int64_t>((tot + 127) / 128, 8192), 128, 0, st>>>(P->d_words, P->d_fvals, theta, x, x_stride, batch, ws.rowtab);
-    P->launches++;
+    g_call.launches++;
   }
   if (P->prefix) {
     const int64_t tot = (int64_t)batch * P->n;
     k_prefix_table<<<(int)std::min<int64_t>((tot + 127) / 128, 8192), 128, 0, st>>>(P->d_words, P->d_fvals, theta, x, x_stride, batch, ws.ptab);
-    P->launches++;
+    g_call.launches++;
   }
   CUDA_TRY(cudaGetLastError());
   const int64_t mtot = (int64_t)batch * std::max(P->slot_total, 1);
   k_zero<<<(int)std::min<int64_t>((mtot + 255) / 256, 4096), 256, 0, st>>>(ws.macc, mtot);
-  P->launches++;
+  g_call.launches++;
   const int L = P->npasses;
   {
     int flags = F_NOFWD | F_STORE_LAM | F_STORE_PSI;
@@ -1036,7 +1042,7 @@ int lsq_bwd_from_state(const lsq_program* Pc, int batch, const double* theta, co
     if (rc) return rc;
     Geometry g = geometry(P, L - 1, MODE_TURN, batch);
     k_reduce_z<<<(batch + 127) / 128, 128, 0, st>>>(ws.zpart, g.cpr, P->n, w, zq, value, batch);
-    P->launches++;
+    g_call.launches++;
     CUDA_TRY(cudaGetLastError());
   }
   for (int i = L - 2; i >= 0; --i) {

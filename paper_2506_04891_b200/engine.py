@@ -24,6 +24,19 @@ from .schedule import compile_circuit
 _STATE_FRACTION = 0.6  # of free device memory usable for psi + lambda
 
 
+def _on_device(fn):
+    """Run an Engine method with its device current: the native calls launch on the current
+    device, with a stream and tables that belong to self.device."""
+    import functools
+
+    @functools.wraps(fn)
+    def wrapper(self, *a, **k):
+        with torch.cuda.device(self.device):
+            return fn(self, *a, **k)
+
+    return wrapper
+
+
 def _ptr(t) -> int | None:
     return None if t is None else t.data_ptr()
 
@@ -99,14 +112,23 @@ class NativeProgram:
                 pass
             self.handle = None
 
-    def workspace(self, batch: int) -> torch.Tensor:
-        ws = self._ws.get(batch)
-        if ws is None:
-            nbytes = int(_native.lib().lsq_workspace_bytes(self.handle, batch))
-            if nbytes < 0:
-                raise ValueError("invalid batch for workspace")
-            ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
-            self._ws = {batch: ws}  # keep one size cached
+    def workspace_bytes(self, batch: int) -> int:
+        nbytes = int(_native.lib().lsq_workspace_bytes(self.handle, batch))
+        if nbytes < 0:
+            raise ValueError("invalid batch for workspace")
+        return nbytes
+
+    def workspace(self, *batches: int) -> torch.Tensor:
+        """One workspace large enough for every chunk size in `batches` (the carve of a chunk
+        depends on its row count through the launch geometry and is not monotone in it, so a
+        short last chunk can need more than a full one). The cached tensor is replaced when a
+        larger one is needed; callers that capture it in a CUDA graph keep their own reference
+        (GradStep), so a replaced workspace stays alive as long as a graph uses it."""
+        nbytes = max(256, max(self.workspace_bytes(b) for b in batches if b > 0))
+        ws = self._ws.get("ws")
+        if ws is None or ws.numel() < nbytes:
+            ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+            self._ws = {"ws": ws}
         return ws
 
     def set_profiling(self, on: bool):
@@ -133,38 +155,33 @@ class Engine:
         self.device = torch.device(device if device is not None else "cuda")
         if self.device.type != "cuda":
             raise ValueError("the engine runs on CUDA devices only")
+        if jit is False or os.environ.get("LSQ_JIT", "1") == "0":
+            raise ValueError("the engine has one kernel family: the per-circuit specialised sm_100a kernels "
+                             "(the run-time interpreting kernel was removed)")
         self.circuit = circuit
         self.n = int(circuit.n)
-        if jit is None:
-            jit = os.environ.get("LSQ_JIT", "1") != "0"
-        if jit and R is None:
-            # specialised kernels: 16 amplitudes per thread per vector once tiles are >= 9
-            # bits (measured best, profiles/r01); the generic kernels keep schedule.default_r
+        if R is None:
+            # 16 amplitudes per thread per vector once tiles are >= 9 bits (measured best,
+            # profiles/r01)
             from .schedule import DEFAULT_M, DEFAULT_R_SPECIALISED, default_r
 
             m = min(self.n, M if M is not None else DEFAULT_M)
             R = DEFAULT_R_SPECIALISED if m >= 9 else default_r(m)
         if prefix is None:
-            prefix = jit and os.environ.get("LSQ_PREFIX", "1") != "0"
-        if prefix and not jit:
-            raise ValueError("the product-state prefix needs the specialised (JIT) kernels")
+            prefix = os.environ.get("LSQ_PREFIX", "1") != "0"
         # trailing diagonal / permutation groups folded into the observable: gradient-type
-        # programs only (same JIT requirement as the prefix)
+        # programs only
         if fold is None:
             fold = bool(prefix) and os.environ.get("LSQ_FOLD", "1") != "0"
-        if fold and not jit:
-            raise ValueError("the folded observable needs the specialised (JIT) kernels")
-        # diagonal gates split out of one-qubit groups when the remainder is cheaper (JIT only:
-        # the structure-aware apply is what makes the remainder cheaper)
+        # diagonal gates split out of one-qubit groups when the remainder is cheaper
         if split is None:
-            split = jit and os.environ.get("LSQ_SPLIT", "1") != "0"
+            split = os.environ.get("LSQ_SPLIT", "1") != "0"
         self.program = compile_circuit(circuit, M=M, R=R, isolate=isolate, prefix=prefix, fold=fold,
                                        split=split)
         self.prefix = bool(self.program.prefix) or bool(self.program.obs)
         self.native = NativeProgram(self.program, self.device)
-        if jit:
-            self.native.attach_jit()
-        self.variant = "jit" if jit else "interp"
+        self.native.attach_jit()
+        self.variant = "jit"
         self.T = self.program.trainable_count
         self.E = self.program.encoding_count
 
@@ -212,6 +229,7 @@ class Engine:
         return cache[key]
 
     # -- forward ----------------------------------------------------------------------------
+    @_on_device
     def forward(self, trainable=None, encoding=None, state=None, batch=None, weights=None, want_z=False):
         """Evolve `state` ((B, 2^n) complex64 CUDA tensor, or None = |0..0> with `batch` rows)
         through the circuit into a NEW tensor. Returns (psi, zq, value)."""
@@ -261,6 +279,7 @@ class Engine:
             return env
         return "ckpt" if self.micro_batch(batch, L) >= min(batch, 16) else "recompute"
 
+    @_on_device
     def fwd_bwd(self, trainable=None, encoding=None, batch=1, weights=None, rows=True,
                 encoding_grads=True, micro_batch=None, buffers=None, checkpoint=None, out=None):
         """Forward from |0..0> plus adjoint backward. Returns a dict of CUDA tensors:
@@ -290,9 +309,11 @@ class Engine:
         else:
             gparts = torch.zeros((nchunk, max(self.T, 1)), **f64)
         def fits(bufs):
-            return (bufs is not None and bufs[0].shape[0] >= mb
-                    and (mode == "recompute" or (bufs[2] is not None and bufs[2].shape[1] >= mb
-                                                 and bufs[2].shape[0] >= L - 1)))
+            if bufs is None or bufs[0].shape[0] < mb:
+                return False
+            if mode == "recompute":  # separate psi and lambda, no checkpoint slots
+                return bufs[2] is None and bufs[0] is not bufs[1]
+            return bufs[2] is not None and bufs[2].shape[1] >= mb and bufs[2].shape[0] >= L - 1
 
         held = self.__dict__.get("_held_buffers")
         if buffers is not None and len(buffers) == 3 and fits(buffers):
@@ -309,7 +330,7 @@ class Engine:
                 ck = None
                 psi = torch.empty_like(lam)
             self._held_buffers = (psi, lam, ck)
-        ws = self.native.workspace(mb)
+        ws = self.native.workspace(mb, batch - (nchunk - 1) * mb)
         lib = _native.lib()
         for c in range(nchunk):
             r0 = c * mb
@@ -336,13 +357,15 @@ class Engine:
             o["grad_sum"].copy_(gsum)
             gsum = o["grad_sum"]
         return {"value": value, "zq": zq, "grads": grows, "grad_sum": gsum, "encoding_grads": erows,
-                "buffers": (psi, lam, ck), "adjoint": mode}
+                "buffers": (psi, lam, ck), "workspace": ws, "adjoint": mode,
+                "native_mode": "ckpt" if ck is not None else "recompute"}
 
     def make_step(self, batch, rows=True, encoding_grads=True, checkpoint=None, graph=None):
         """A reusable forward+adjoint step with static device inputs/outputs, replayed as one
         CUDA graph (the whole launch sequence: tables, passes, reductions, contraction)."""
         return GradStep(self, batch, rows, encoding_grads, checkpoint, graph)
 
+    @_on_device
     def backward_from_state(self, trainable, encoding, final_state, weights=None):
         """Adjoint sweep from a given final state (reference backward_sweep)."""
         if self.prefix:
@@ -422,9 +445,12 @@ class GradStep:
         if graph:
             torch.cuda.synchronize(dev)
             g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
+            with torch.cuda.device(dev), torch.cuda.graph(g):
                 self.out = self._call()
             self.graph = g
+        # the graph holds raw addresses of the workspace and state buffers it captured: keep
+        # them alive for the step's lifetime, whatever later calls on the engine allocate
+        self._captured = (self.out.get("workspace"), self.out.get("buffers"))
 
     def _call(self):
         e = self.eng

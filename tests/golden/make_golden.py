@@ -142,6 +142,22 @@ def save_known_answers():
         p = rng.uniform(-1.5, 1.5, (len(pos), k)) if k else None
         kv[f"layer_{name}_params"] = p if p is not None else np.zeros((0,))
         kv[f"layer_{name}"] = layer_unitary(layer, 4, p)
+    # X layers and GPI xor-flips (permutation/antidiagonal index maps, bit-exact tests);
+    # fixed angles so these keys do not consume the rng stream above
+    from layersim.kernels import _flip_mask
+
+    for n in (3, 5):
+        kv[f"sigma_x_all_{n}"] = compose_permutation(ref.Layer(ref.GateKind.X, ref.all_qubits()), n).sigma
+    kv["sigma_x_explicit_0_2_4"] = compose_permutation(
+        ref.Layer(ref.GateKind.X, ref.explicit((0,), (2,))), 4).sigma
+    gpi = {"all_4": (ref.all_qubits(), 4), "explicit_1_3_5": (ref.explicit((1,), (3,)), 5)}
+    for name, (pat, n) in gpi.items():
+        layer = ref.Layer(ref.GateKind.GPI, pat, ref.Role.TRAINABLE)
+        pos = ref.positions(layer, n)
+        kv[f"gpi_flip_mask_{name}"] = np.int64(_flip_mask(pos, n))
+        for tag, p in (("zero", np.zeros((len(pos), 1))), ("phase", np.linspace(0.05, 0.4, len(pos))[:, None])):
+            kv[f"layer_gpi_{name}_{tag}_params"] = p
+            kv[f"layer_gpi_{name}_{tag}"] = layer_unitary(layer, n, p)
     path = os.path.join(HERE, "known_answers.npz")
     np.savez_compressed(path, **kv)
     print("known answers ->", path)

@@ -68,3 +68,33 @@ def test_jit_uses_toolkit_nvrtc_not_first_loaded():
     assert not err, err
     maj, mnr = map(int, ver.split("."))
     assert (maj, mnr) >= (12, 9), (path, ver)
+
+
+def test_program_artifact_roundtrip_and_loader_errors(tmp_path):
+    """Artifact format (host side) round-trips; the C loader rejects malformed files with the
+    documented status codes before touching the device."""
+    from paper_2506_04891_b200 import artifact
+    from paper_2506_04891_b200.configs import make_workload
+    from paper_2506_04891_b200.schedule import compile_circuit
+
+    wl = make_workload(2, n=10, batch=2)
+    prog = compile_circuit(wl.circuit, M=8, R=4, prefix=True, fold=True, split=True)
+    blob = artifact.encode(prog)
+    d = artifact.decode(blob)
+    assert list(d["words"]) == list(prog.words)
+    assert len(d["kernels"]) == 2 * len(prog.passes)
+    assert all(src.count("__global__") >= 1 for _, _, _, src, _ in d["kernels"])
+    if not os.path.exists(_native.LIB_PATH):
+        return
+    lib = _native.load_library()
+    h = ctypes.c_void_p()
+    bad = tmp_path / "bad.lsqp"
+    bad.write_bytes(b"NOPE" + blob[4:])
+    assert lib.lsq_program_load(str(bad).encode(), None, ctypes.byref(h)) == 1
+    ver = tmp_path / "ver.lsqp"
+    ver.write_bytes(blob[:4] + (2).to_bytes(4, "little") + blob[8:])
+    assert lib.lsq_program_load(str(ver).encode(), None, ctypes.byref(h)) == 2
+    trunc = tmp_path / "trunc.lsqp"
+    trunc.write_bytes(blob[: len(blob) // 2])
+    assert lib.lsq_program_load(str(trunc).encode(), None, ctypes.byref(h)) == 1
+    assert b"truncated" in lib.lsq_last_error() or b"corrupt" in lib.lsq_last_error()
