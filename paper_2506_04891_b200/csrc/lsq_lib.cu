@@ -3,6 +3,7 @@
 // deterministic fp64 reductions, coupling contraction).
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <nvtx3/nvToolsExt.h>
 #include <limits.h>
 #include <nvrtc.h>
 #include <stdlib.h>
@@ -488,6 +489,14 @@ int launch_pass(const lsq_program* P, int pi_idx, int mode, int flags, int batch
   A.part = ws.part;
   A.zpart = ws.zpart;
   CallState& C = g_call;
+  // NVTX range per pass launch ("lsq p<pass> <mode>"): host-side, free without an attached tool
+  static const char* const kModeName[3] = {"fwd", "turn", "adj"};
+  char nvtx_name[32];
+  snprintf(nvtx_name, sizeof nvtx_name, "lsq p%d %s", pi_idx, kModeName[mode]);
+  nvtxRangePushA(nvtx_name);
+  struct NvtxPop {
+    ~NvtxPop() { nvtxRangePop(); }
+  } nvtx_pop;
   if (C.profiling) {
     while ((int)C.ev.size() < 2 * (C.ev_used + 1)) {
       cudaEvent_t e;

@@ -293,7 +293,7 @@ def split_diagonal(groups: list[Group], keep=(), drop_phase: bool = False) -> li
         # a diagonal part followed by a non-diagonal one runs where its wire is a register bit
         # (one complex phase per amplitude, charged 4); trailing diagonal parts are deferred
         split = g.gid not in keep and g.arity == 1 and len(parts) > 1
-        if split:
+        if split and _os.environ.get("LSQ_SPLIT_FORCE") != "1":
             cost = sum(_apply_cost(Group(0, g.wires, p), drop_phase) if not p[0][0].diag else
                        (4 if k < len(parts) - 1 else 0) for k, p in enumerate(parts))
             split = cost < _apply_cost(g, drop_phase)

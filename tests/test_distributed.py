@@ -70,3 +70,49 @@ def test_gloo_world2_allreduce_matches_single_process():
         np.testing.assert_allclose(gs, ref["grads"].sum(0), atol=1e-12)
         np.testing.assert_allclose(grads, ref["grads"][s:e], atol=1e-12)
     assert out[0][:2] == (0, 3) and out[1][:2] == (3, 5)
+
+
+def _worker_small(rank, world, port, out):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2506_04891_b200.configs import make_workload
+    from paper_2506_04891_b200.distributed import data_parallel_gradient
+
+    wl = make_workload(5, n=5, batch=1)
+    try:
+        data_parallel_gradient(wl.circuit, wl.theta, wl.x, wl.weights, step_fn=_oracle_step)
+        out[rank] = "no error"
+    except ValueError as e:
+        out[rank] = f"ValueError: {e}"
+    # an encoding-free circuit: `batch` identical rows sharded like encoded ones
+    from paper_2506_04891_b200.circuits import Circuit, Layer, Role, all_qubits
+    from paper_2506_04891_b200.gates import GateKind
+
+    c = Circuit(3, [Layer(GateKind.RY, all_qubits(), Role.TRAINABLE)])
+    (s, e), res, gs = data_parallel_gradient(c, np.array([0.3, 0.5, 0.7]), None, None, step_fn=_oracle_step,
+                                             batch=4)
+    out[f"{rank}_free"] = (s, e, gs)
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_small_batch_errors_everywhere_no_hang():
+    """world > batch raises the same ValueError on EVERY rank before any collective (no rank
+    is left blocked in the all-reduce); an encoding-free circuit shards its `batch` rows."""
+    from oracle import layersim_oracle as orc
+    from paper_2506_04891_b200.circuits import Circuit, Layer, Role, all_qubits
+    from paper_2506_04891_b200.gates import GateKind
+
+    world = 2
+    port = _free_port()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.start_processes(_worker_small, args=(world, port, out), nprocs=world, start_method="fork")
+    for r in range(world):
+        assert out[r].startswith("ValueError") and "cannot be sharded" in out[r]
+    c = Circuit(3, [Layer(GateKind.RY, all_qubits(), Role.TRAINABLE)])
+    ref = orc.gradient(c, np.array([0.3, 0.5, 0.7]), None, batch=4)
+    assert out["0_free"][:2] == (0, 2) and out["1_free"][:2] == (2, 4)
+    for r in range(world):
+        np.testing.assert_allclose(out[f"{r}_free"][2], ref["grads"].sum(0), atol=1e-12)

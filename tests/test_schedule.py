@@ -163,3 +163,34 @@ def test_diagonal_runs_are_sunk():
             runs = sum(1 for i, d in enumerate(kinds) if d and (i == 0 or not kinds[i - 1]))
             nd_after = [i for i, d in enumerate(kinds) if not d]
             assert runs <= max(1, len(nd_after)), (kinds,)
+
+
+REF_SRC = "/root/reference/pkg/src"
+
+
+@pytest.mark.skipif(not __import__("os").path.isdir(REF_SRC), reason="reference sources absent (GPU box)")
+@pytest.mark.parametrize("cfg", [2, 3, 4])
+def test_reference_circuit_objects_compile_by_duck_typing(cfg):
+    """The drop-in accepts the REFERENCE's own layersim.Circuit objects: compiled by
+    schedule.compile_circuit and interpreted on the CPU, they give the oracle's results for our
+    equivalent circuit (the reference package is imported read-only, in this container only)."""
+    import importlib
+    import sys
+
+    sys.path.insert(0, REF_SRC)
+    try:
+        ls = importlib.import_module("layersim")
+    finally:
+        sys.path.remove(REF_SRC)
+    wl = make_workload(cfg, n=6, batch=3)
+    layers = []
+    for layer in wl.circuit.layers:
+        pat = ls.WirePattern(ls.PatternKind(layer.pattern.kind.value), layer.pattern.wires)
+        role = None if layer.role is None else ls.Role(layer.role.value)
+        layers.append(ls.Layer(ls.GateKind(layer.gate.value), pat, role, layer.values))
+    rc = ls.Circuit(wl.n, layers)
+    assert type(rc).__module__.startswith("layersim")
+    prog = S.compile_circuit(rc, M=5, R=2)
+    res = Emulator(prog).gradient(wl.theta, wl.x, 3, wl.weights)
+    ref = orc.gradient(wl.circuit, wl.theta, wl.x, batch=3, weights=wl.weights)
+    _cmp(res, ref)
