@@ -258,7 +258,9 @@ class RefCPU:
         circ = wl.circuit if self.nblocks is None else _sub_circuit(self.cfg, wl.circuit, self.nblocks)
         b = max(e - s for sh in self.shards for s, e in sh)
         t0 = time.perf_counter()
-        plan = build_plan(_to_ref_circuit(ls, circ), b, Objective.FORWARD_BACKWARD)
+        # reps=3, warmup=1 instead of the defaults 10/3: the n=22 build takes ~4 min with the
+        # defaults on one core; both settings pick the same kernels for the cfg4 circuit at n=16
+        plan = build_plan(_to_ref_circuit(ls, circ), b, Objective.FORWARD_BACKWARD, reps=3, warmup=1)
         return serialize_plan(plan), time.perf_counter() - t0
 
     def describe(self):

@@ -480,6 +480,73 @@ def _emit_tan_rot(w, P, k, g, nvec, dagger, classes):
     P.tan_count += 1
 
 
+EULER_TAN = os.environ.get("LSQ_EULER_TAN", "1") != "0"
+# groups whose |U00| varies with the parameters need the uniform fallback branch (adjoint only)
+EULER_BRANCH = os.environ.get("LSQ_EULER_BRANCH", "1") != "0"
+_MAG_CACHE: dict = {}
+
+
+def u00_const_mag(grp, samples: int = 6):
+    """|U00| of a one-qubit group when it is the same for every parameter value (RZ.SX.RZ,
+    GPI2.GPI: 1/sqrt2), else None. Such groups take the Euler tangent form without a branch."""
+    from .gates import gate_matrix
+
+    key = tuple((g.kind, tuple(g.src), tuple(g.fixed)) for g, _ in grp.gates)
+    if key in _MAG_CACHE:
+        return _MAG_CACHE[key]
+    rng = np.random.default_rng(4321)
+    mags = []
+    for _ in range(samples):
+        U = np.eye(2, dtype=complex)
+        for g, _r in grp.gates:
+            k = GATE_TRAITS[g.kind].param_count
+            prm = [g.fixed[j] if g.src[j] == S.FIXED_SRC else float(rng.uniform(-3.0, 3.0)) for j in range(k)]
+            U = (gate_matrix(g.kind, prm) if k else gate_matrix(g.kind)) @ U
+        mags.append(abs(U[0, 0]))
+    m = mags[0] if (max(mags) - min(mags) < 1e-9 and mags[0] >= 0.1) else None
+    _MAG_CACHE[key] = m
+    return m
+
+
+def _emit_euler_tan(w, P, k, g, nvec, dagger, classes, branch):
+    """General one-qubit group U = e^{i d} diag(1, e^{ia}) R(b) diag(1, e^{ig}) (R = [[c, -s],
+    [s, c]], global phase dropped: gradient programs only) on register bit k, with the rotation
+    in tangent form R / c = [[1, -t], [t, 1]]: per pair a phase on one member, two single-FFMA2
+    outputs and a phase on one output -- 6 packed ops instead of 8; the vectors carry the
+    run-time scale rho_ *= c = |U00|. Adjoint: U^+ = diag(1, e^{-ig}) R(-b) diag(1, e^{-ia}).
+    The group table entry holds U (floats 0..7, row-major re, im) and, from the fp64 group-table
+    kernel (lsq_common.cuh group_table_entry), c, t, e^{ia}, e^{ig} (floats 8..13). `branch`:
+    |U00| may vanish, so c < TAN_TH takes the direct form (uniform branch)."""
+    w(f"{{ const float c_ = {g}[8], t_ = {g}[9], nt_ = -t_;")
+    w(f"  const float2 ea_ = make_float2({g}[10], {g}[11]), eg_ = make_float2({g}[12], {g}[13]);")
+    if branch:
+        w(f"  if (c_ >= {TAN_TH}f) {{")
+    for q in range(nvec):
+        for i in range(1 << P.R):
+            if (i >> k) & 1:
+                continue
+            j = i | (1 << k)
+            if not dagger:
+                w(f"    {{ const float2 x0 = v[{q}][{i}], x1 = cm(eg_.x, eg_.y, v[{q}][{j}]); "
+                  f"v[{q}][{i}] = fx(x1, nt_, x0); v[{q}][{j}] = cm(ea_.x, ea_.y, fx(x0, t_, x1)); }}")
+            else:
+                w(f"    {{ const float2 x0 = v[{q}][{i}], x1 = cm(ea_.x, -ea_.y, v[{q}][{j}]); "
+                  f"v[{q}][{i}] = fx(x1, t_, x0); v[{q}][{j}] = cm(eg_.x, -eg_.y, fx(x0, nt_, x1)); }}")
+    w("    rho_ *= c_;")
+    if branch:
+        # the global phase e^{-i d} dropped here is tracked (phc_): the direct form of the else
+        # branch, the forward kernels and the checkpoints keep it, so stored vectors must too
+        w(f"    phc_ = cm({g}[14], {'-' if dagger else ''}{g}[15], phc_);")
+        P.ph_live = True
+        w("  } else {")
+        for q in range(nvec):
+            _emit_u1_struct(w, f"v[{q}]", k, P.R, classes, g, dagger)
+        w("  }")
+    w("}")
+    P.rho_live = True
+    P.tan_count += 1
+
+
 def _renorm_rho(w, P, nvec):
     """Multiply the run-time scale back into the amplitudes (range guard, branch merges)."""
     if not P.rho_live:
@@ -965,8 +1032,16 @@ def _emit_ops(w, P, ph_idx, mode_bwd, nv):
             elif kind == S.OP_U1:
                 classes = u1_structure(grp)[0]
                 w(f"{{ const float* g_ = s_mat + {moff};")
+                general = all(c == "c" for row in classes for c in row)
+                cmag = u00_const_mag(grp) if general else None
                 if TAN_ROT and P.tan_ok and is_rotation(grp):
                     _emit_tan_rot(w, P, bits[0], "g_", nv if mode_bwd else 1, mode_bwd, classes)
+                    if P.tan_count >= TAN_RENORM:
+                        _renorm_rho(w, P, nv if mode_bwd else 1)
+                elif (EULER_TAN and general and P.drop_phase and P.walsh_diag
+                      and (cmag is not None or (P.tan_ok and EULER_BRANCH))):
+                    _emit_euler_tan(w, P, bits[0], "g_", nv if mode_bwd else 1, mode_bwd, classes,
+                                    branch=cmag is None)
                     if P.tan_count >= TAN_RENORM:
                         _renorm_rho(w, P, nv if mode_bwd else 1)
                 else:
@@ -1093,6 +1168,9 @@ class _Rot:
 
 
 SMEM_LIMIT = 227 * 1024
+# prefetch stage in the swizzled order of the exchange buffers (LSQ_STAGE_SWZ=0: natural order,
+# round 1 -- its phase-layout reads were bank-conflicted: ncu 4.4e8 excess wavefronts in cfg4 p1)
+STAGE_SWZ = os.environ.get("LSQ_STAGE_SWZ", "1") != "0"
 
 
 def generic_smem_bytes(prog, pi: int) -> int:
@@ -1128,6 +1206,7 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
     P.walsh = []  # (slot, arity, components) of diagonal couplings kept as Walsh sums
     P.sc = [1.0, 1.0]  # deferred (compile-time) scale of psi and lambda: computed = true x sc
     P.rho_live = False  # run-time scale rho_ (tangent-form rotations) may differ from 1
+    P.ph_live = False  # run-time global phase phc_ (branching Euler groups) may differ from 1
     P.tan_count = 0
     # tangent-form rotations in the adjoint kernels only: measured -2% there, +3% in the forward
     # and turnaround kernels (the uniform fallback branch costs them their scheduling freedom)
@@ -1234,7 +1313,11 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
     cth_terms = [f"(((uint32_t)tid >> {jj}) & 1u) << {P.pbit[jj + 1]}" for jj in range(tid_bits)]
     w(f"const uint32_t cth = {' | '.join(cth_terms) if cth_terms else '0u'};")
     w(f"const bool cp_on = tid < {nchunk};")
-    w("(void)cth; (void)cp_on;")
+    # the stage holds the tile in the exchange buffers' swizzled order (S is XOR-linear and
+    # keeps every 16-byte chunk whole), so reading it in any phase layout is as conflict-free
+    # as an exchange; the writer's per-thread part of the swizzled chunk address is hoisted
+    w(f"const uint32_t cst_ = {'swz(2u * (tid & ' + str((1 << tid_bits) - 1) + '))' if STAGE_SWZ else '2u * (tid & ' + str((1 << tid_bits) - 1) + ')'};")
+    w("(void)cth; (void)cp_on; (void)cst_;")
     ld_vecs = [(0, "A.psi_in"), (1, "A.lam")] if mode == MODE_BWD else [(0, "A.psi_in")]
     if mode == MODE_FWD:
         w("const bool do_load = !(flags & PF_SYNTH);")
@@ -1252,8 +1335,8 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
             for jj in range(per_thr):
                 loc = 2 * (jj << tid_bits)
                 phys = sum(1 << P.pbit[b] for b in range(P.M) if (loc >> b) & 1)
-                w(f"cp_async16(s_stage + {vi * (1 << P.M) + loc} + 2 * (tid & {(1 << tid_bits) - 1}), "
-                  f"{ptr} + nb + (cth | {phys}u));")
+                sl = S_swz(loc) if STAGE_SWZ else loc
+                w(f"cp_async16(s_stage + {vi * (1 << P.M)} + (cst_ ^ {sl}u), {ptr} + nb + (cth | {phys}u));")
         w.end()
 
     def emit_stage_read(k):
@@ -1263,11 +1346,17 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
             if pr is not None:  # natural order: the pair on local bit 0 is adjacent
                 for i, j in pr:
                     loc = sum(1 << ph.regs[b] for b in range(P.R) if (i >> b) & 1)
-                    w(f"ld_pair(s_stage, {vi * (1 << P.M)} + (tp{k} | {loc}u), v[{vi}][{i}], v[{vi}][{j}]);")
+                    if STAGE_SWZ:
+                        w(f"ld_pair(s_stage, {vi * (1 << P.M)} + (st{k} ^ {S_swz(loc)}u), v[{vi}][{i}], v[{vi}][{j}]);")
+                    else:
+                        w(f"ld_pair(s_stage, {vi * (1 << P.M)} + (tp{k} | {loc}u), v[{vi}][{i}], v[{vi}][{j}]);")
                 continue
             for i in range(P.NR):
                 loc = sum(1 << ph.regs[b] for b in range(P.R) if (i >> b) & 1)
-                w(f"v[{vi}][{i}] = s_stage[{vi * (1 << P.M)} + (tp{k} | {loc}u)];")
+                if STAGE_SWZ:
+                    w(f"v[{vi}][{i}] = s_stage[{vi * (1 << P.M)} + (st{k} ^ {S_swz(loc)}u)];")
+                else:
+                    w(f"v[{vi}][{i}] = s_stage[{vi * (1 << P.M)} + (tp{k} | {loc}u)];")
 
     if prefetch:
         w.block("if (do_load && t0 < t_end)")
@@ -1289,7 +1378,8 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
     w("const size_t base = rowbase + tbase;")
     w(f"float2 v[{nv}][{P.NR}];")
     w("float rho_ = 1.f;  // run-time deferred scale of the tile's vectors (true = computed x rho_)")
-    w("(void)rho_;")
+    w("float2 phc_ = make_float2(1.f, 0.f);  // run-time global phase (true = computed x rho_ x phc_)")
+    w("(void)rho_; (void)phc_;")
 
     def emit_load(k):
         """wait for this tile's prefetch, move it to registers (layout k), prefetch the next;
@@ -1662,7 +1752,8 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
             f = _f(c) if abs(c - 1.0) >= 1e-15 else None
             if P.rho_live:
                 f = "rho_" if f is None else f"({f} * rho_)"
-            return f"v[{q}][{i}]" if f is None else f"mx(v[{q}][{i}], {f})"
+            x = f"v[{q}][{i}]" if f is None else f"mx(v[{q}][{i}], {f})"
+            return f"cm(phc_.x, phc_.y, {x})" if P.ph_live else x
         if what == "psi":
             w.block("if (flags & PF_STORE_PSI)")
             for i in range(P.NR):
@@ -1684,6 +1775,11 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
         if f is not None:
             for i in range(P.NR):
                 w(f"v[{q}][{i}] = mx(v[{q}][{i}], {f});")
+        if P.ph_live:  # only lambda is renormalized (prefix couplings): psi is dead by then
+            for i in range(P.NR):
+                w(f"v[{q}][{i}] = cm(phc_.x, phc_.y, v[{q}][{i}]);")
+            w("phc_ = make_float2(1.f, 0.f);")
+            P.ph_live = False
         P.sc[q] = 1.0
         if P.rho_live:
             w("rho_ = 1.f;")

@@ -310,6 +310,26 @@ __device__ inline void group_table_entry(const int* W, int gid, const double* fv
       out[2 * e] = (float)U[e].r;
       out[2 * e + 1] = (float)U[e].i;
     }
+    if (d == 2) {
+      // Euler / tangent form of the one-qubit kernels (codegen._emit_euler_tan): U = e^{i d}
+      // diag(1, e^{ia}) [[c, -s], [s, c]] diag(1, e^{ig}) -> c = |U00|, t = s / c,
+      // e^{ia} = U10 conj(U00) / |.|, e^{ig} = U11 conj(U00) e^{-ia} / c^2 (fp64 here, once)
+      const double c2 = U[0].r * U[0].r + U[0].i * U[0].i, c = sqrt(c2);
+      cd ea = mk(U[2].r * U[0].r + U[2].i * U[0].i, U[2].i * U[0].r - U[2].r * U[0].i);
+      const double ns = sqrt(ea.r * ea.r + ea.i * ea.i);
+      ea = ns > 1e-300 ? cscale(ea, 1.0 / ns) : mk(1.0, 0.0);
+      cd dd = mk(U[3].r * U[0].r + U[3].i * U[0].i, U[3].i * U[0].r - U[3].r * U[0].i);
+      dd = c2 > 1e-300 ? cscale(dd, 1.0 / c2) : mk(1.0, 0.0);
+      const cd eg = cmulx(dd, cconj(ea));
+      out[8] = (float)c;
+      out[9] = c2 > 1e-300 ? (float)(ns / c2) : 0.f;  // |U10| |U00| / |U00|^2 = s / c
+      out[10] = (float)ea.r;
+      out[11] = (float)ea.i;
+      out[12] = (float)eg.r;
+      out[13] = (float)eg.i;
+      out[14] = c2 > 1e-300 ? (float)(U[0].r / c) : 1.f;  // e^{i d} = U00 / |U00|
+      out[15] = c2 > 1e-300 ? (float)(U[0].i / c) : 0.f;
+    }
   }
 }
 

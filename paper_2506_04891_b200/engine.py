@@ -289,7 +289,8 @@ class Engine:
         mode = self.adjoint_mode(batch, checkpoint)
         L = len(self.program.passes)
         nvec = L if mode == "ckpt" else 2
-        mb = micro_batch or self.micro_batch(batch, nvec)
+        env_mb = int(os.environ.get("LSQ_MICRO_BATCH", "0"))  # experiments (L2-resident micro-batches)
+        mb = micro_batch or (min(env_mb, batch) if env_mb > 0 else self.micro_batch(batch, nvec))
         self.last_micro_batch, self.last_adjoint = mb, mode
         dev = self.device
         f64 = dict(dtype=torch.float64, device=dev)

@@ -160,7 +160,8 @@ class Group:
     def mat_floats(self) -> int:
         if self.diag:
             return 1 << self.arity  # fixed-point phase angles, one word each
-        return 8 if self.arity == 1 else 32
+        # one-qubit: U (8 floats) + its Euler / tangent form (c, t, e^{ia}, e^{ig}, pad)
+        return 16 if self.arity == 1 else 32
 
     @property
     def perm_ops(self):

@@ -97,12 +97,23 @@ def test_cfg1_full():
     check(res, load_golden("cfg1_full"))
 
 
+def precision_model_tol(circ, theta, x, w, ref, batch):
+    """A2 bound for a random circuit: 1e-4, or twice the A2 error of the reference algorithm run
+    in complex64 (oracle dtype=np.complex64) where that precision model itself breaks 1e-4."""
+    r32 = orc.gradient(circ, theta, x, batch=batch, weights=w, dtype=np.complex64)
+    c64 = a2_errors(_angles(r32["grads"], r32["encoding_grads"]), _angles(ref["grads"], ref["encoding_grads"]))[0]
+    c64s = a2_errors(r32["grads"].sum(0), ref["grads"].sum(0))[0]
+    return max(G_REL, 2 * c64, 2 * c64s), f"complex64 precision model A2 err {c64:.2e} (sum {c64s:.2e})"
+
+
 @pytest.mark.parametrize("c", range(6))
 def test_random_circuits(c):
     gold = load_golden("random_circuits")
     circ = rebuild_random(gold[f"c{c}_spec"])
+    ref = {k[len(f"c{c}_"):]: v for k, v in gold.items() if k.startswith(f"c{c}_")}
     res = gradient(circ, gold[f"c{c}_theta"], gold[f"c{c}_x"], batch=3, weights=gold[f"c{c}_w"])
-    check(res, {k[len(f"c{c}_"):]: v for k, v in gold.items() if k.startswith(f"c{c}_")})
+    tol, note = precision_model_tol(circ, gold[f"c{c}_theta"], gold[f"c{c}_x"], gold[f"c{c}_w"], ref, 3)
+    check(res, ref, tol=tol, note=note, what=f"golden_random{c}")
 
 
 @pytest.mark.parametrize("tag,cfg", [("cfg2_rows4", 2), ("cfg3_rows2", 3), ("cfg4_rows1", 4), ("cfg5_rows1", 5)])
@@ -473,9 +484,13 @@ def test_random_circuits_multipass(seed, M):
     w = rng.normal(size=10)
     res = gradient(circ, theta, x, batch=3, weights=w, plan=plan_for_tile_bits(circ, 3, M))
     ref = orc.gradient(circ, theta, x, batch=3, weights=w)
-    r32 = orc.gradient(circ, theta, x, batch=3, weights=w, dtype=np.complex64)
-    c64 = a2_errors(_angles(r32["grads"], r32["encoding_grads"]), _angles(ref["grads"], ref["encoding_grads"]))[0]
-    c64s = a2_errors(r32["grads"].sum(0), ref["grads"].sum(0))[0]
-    tol = max(G_REL, 2 * c64, 2 * c64s)
-    check(res, ref, tol=tol, note=f"complex64 precision model A2 err {c64:.2e} (sum {c64s:.2e})",
-          what=f"random{seed}_M{M}")
+    g_ref = _angles(ref["grads"], ref["encoding_grads"])
+    if np.abs(g_ref).max() < 1e-12:  # every gradient structurally zero (seed 10): absolute check
+        g = _angles(res.grads, res.encoding_grads)
+        PARITY_LOG.append({"what": f"random{seed}_M{M}", "abs": float(np.abs(g).max()), "tol": 1e-6,
+                           "note": "structurally zero gradients: absolute bound"})
+        assert np.abs(g).max() <= 1e-6
+        np.testing.assert_allclose(res.zq, ref["zq"], atol=Z_TOL)
+        return
+    tol, note = precision_model_tol(circ, theta, x, w, ref, 3)
+    check(res, ref, tol=tol, note=note, what=f"random{seed}_M{M}")
