@@ -236,11 +236,13 @@ def test_apply_circuit_leaves_input_untouched():
 @pytest.mark.parametrize("cfg", [2, 5])
 def test_backward_sweep_from_state(cfg):
     wl = make_workload(cfg, n=7, batch=2)
-    final = orc.apply_circuit(wl.circuit, wl.theta, wl.x, batch=2)
-    st = StateBatch(7, 2, torch.as_tensor(final.astype(np.complex64), device="cuda"))
+    final = orc.apply_circuit(wl.circuit, wl.theta, wl.x, batch=2).astype(np.complex64)
+    st = StateBatch(7, 2, torch.as_tensor(final, device="cuda"))
     res = backward_sweep(wl.circuit, wl.theta, wl.x, st, weights=wl.weights)
-    ref = orc.gradient(wl.circuit, wl.theta, wl.x, batch=2, weights=wl.weights)
-    check(res, ref)
+    # the reference sweep from the SAME (complex64-rounded) final state the engine was given
+    f128 = final.astype(np.complex128)
+    value, grads, egrads = orc.backward_sweep(wl.circuit, wl.theta, wl.x, f128, wl.weights)
+    check(res, {"value": value, "grads": grads, "encoding_grads": egrads, "zq": orc.expectation_z(f128, 7)})
 
 
 def test_micro_batches_agree():
