@@ -22,6 +22,7 @@ import statistics
 import subprocess
 import sys
 import time
+import warnings
 
 import numpy as np
 
@@ -570,11 +571,23 @@ def run_ours(args, world, rank, local):
     wl, r0, r1, gbatch, scaling = _workload_rows(cfg, world, rank, args.batch)
     b = r1 - r0
     n = wl.n
-    # tile exponent: measured by the planner on a bounded row sample (plan build excluded from
-    # the timed region, as the reference's bench does), unless --M is given
-    plan, tile_choice = None, None
-    if args.M is None:
-        from paper_2506_04891_b200.planner import Objective, choose_tile_bits, plan_for_tile_bits
+    # the per-layer CUDA-variant plan: the one build_plan made for this config on a B200
+    # (profiles/plans/cfg<C>.json, profiles/build_plans.py) when present, else the tile exponent
+    # measured here by choose_tile_bits on a bounded row sample (plan build is excluded from the
+    # timed region, as in the reference's bench); --M forces an all-FUSED plan
+    from paper_2506_04891_b200.planner import KernelKind, load_plan, plan_for_tile_bits
+
+    plan, tile_choice, plan_src = None, None, None
+    plan_path = os.path.join(ROOT, "profiles", "plans", f"cfg{cfg}.json")
+    if args.M is not None:
+        plan, plan_src = plan_for_tile_bits(wl.circuit, b, args.M), f"--M {args.M}"
+    elif os.path.exists(plan_path) and not args.no_plan:
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")  # machine id of the box that built it
+            plan = load_plan(plan_path)
+        plan_src = os.path.relpath(plan_path, ROOT)
+    else:
+        from paper_2506_04891_b200.planner import Objective, choose_tile_bits
 
         prow = max(1, min(b, (2 << 30) // (8 << wl.n)))
         M_best, st = choose_tile_bits(wl.circuit, prow, Objective.FORWARD_BACKWARD, device=dev)
@@ -585,13 +598,14 @@ def run_ours(args, world, rank, local):
             dist.broadcast(mt, src=0)
             M_best = int(mt.item())
         tile_choice = {"rows": prow, "ms": {str(m): round(v.mean_seconds * 1e3, 3) for m, v in st.items()}}
-        plan = plan_for_tile_bits(wl.circuit, b, M_best)
-        args.M = M_best
-    else:
-        from paper_2506_04891_b200.planner import plan_for_tile_bits
+        plan, plan_src = plan_for_tile_bits(wl.circuit, b, M_best), "choose_tile_bits"
+    from paper_2506_04891_b200.core import plan_kernels
 
-        plan = plan_for_tile_bits(wl.circuit, b, args.M)  # the e2e leg compiles the same tiling
-    eng = Engine(wl.circuit, device=dev, M=args.M, R=args.R)
+    kinds = plan_kernels(wl.circuit, plan)  # validates the plan against the circuit
+    sel = lambda kk: [i for i, k in enumerate(kinds) if k is kk]  # noqa: E731
+    args.M = plan.tile_bits
+    eng = Engine(wl.circuit, device=dev, M=args.M, R=args.R, isolate=sel(KernelKind.ISOLATED),
+                 direct=sel(KernelKind.DIRECT), split_layers=sel(KernelKind.SPLIT))
     ck = None if args.checkpoint is None else bool(args.checkpoint)
     gate = None
     if args.batch is None:  # BASELINE workloads only (golden rows are the first rows of the batch)
@@ -754,7 +768,8 @@ def run_ours(args, world, rank, local):
                    "rows_per_gpu": b, "micro_batch": mb, "adjoint": eng.last_adjoint,
                    "parallelism": f"dp{world}",
                    "passes": len(eng.program.passes), "tile_bits": eng.program.passes[0].M,
-                   "tile_bits_choice": tile_choice,
+                   "tile_bits_choice": tile_choice, "plan": plan_src,
+                   "plan_variants": {k.value: sum(1 for x in kinds if x is k) for k in set(kinds)},
                    "cuda_graph": gstep.graph is not None,
                    "reg_bits": eng.program.passes[0].R, "variant": eng.variant,
                    "l2": f"working set {2 * b * (8 << n) / 2**20:.0f} MiB (psi+lambda) vs 126 MB L2"
@@ -786,6 +801,7 @@ def main():
     ap.add_argument("--R", type=int, default=None, help="register bits per thread")
     ap.add_argument("--batch", type=int, default=None, help="experiments: rows per GPU (not a bench line)")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of a CUDA graph")
+    ap.add_argument("--no-plan", action="store_true", help="ignore profiles/plans/cfg<C>.json (tile choice only)")
     ap.add_argument("--checkpoint", type=int, default=None, choices=[0, 1],
                     help="adjoint with forward checkpoints (1) or in-place un-computation (0); default: engine")
     args = ap.parse_args()

@@ -94,7 +94,7 @@ def _build_parser():
     g = s.add_mutually_exclusive_group(required=True)
     g.add_argument("--circuit", help="reference circuit JSON file")
     g.add_argument("--config", type=int, choices=[1, 2, 3, 4, 5], help="a BASELINE config circuit")
-    s.add_argument("--plan", default=None, help="plan JSON (tile exponent, isolated layers)")
+    s.add_argument("--plan", default=None, help="plan JSON (tile exponent, per-layer variants)")
     s.add_argument("--gradient", action="store_true",
                    help="gradient program (synthesized |0..0> prefix, folded observable)")
     s.add_argument("--out", required=True)
@@ -160,9 +160,10 @@ def _cmd_compile(args) -> int:
     if R is None:
         m = min(circuit.n, M if M is not None else DEFAULT_M)
         R = DEFAULT_R_SPECIALISED if m >= 9 else default_r(m)
-    isolate = [] if plan is None else [i for i, k in enumerate(plan.assignments) if k is KernelKind.ISOLATED]
-    prog = compile_circuit(circuit, M=M, R=R, isolate=isolate, prefix=args.gradient, fold=args.gradient,
-                           split=True)
+    sel = lambda kk: [] if plan is None else [i for i, k in enumerate(plan.assignments) if k is kk]  # noqa: E731
+    prog = compile_circuit(circuit, M=M, R=R, isolate=sel(KernelKind.ISOLATED), prefix=args.gradient,
+                           fold=args.gradient, split=True, direct=sel(KernelKind.DIRECT),
+                           split_layers=sel(KernelKind.SPLIT))
     size = artifact.write(prog, args.out)
     print(f"wrote {args.out}: n={circuit.n}, {len(prog.passes)} passes, {size} bytes")
     return 0

@@ -1034,12 +1034,13 @@ def _emit_ops(w, P, ph_idx, mode_bwd, nv):
                 w(f"{{ const float* g_ = s_mat + {moff};")
                 general = all(c == "c" for row in classes for c in row)
                 cmag = u00_const_mag(grp) if general else None
-                if TAN_ROT and P.tan_ok and is_rotation(grp):
+                direct = any(g.layer in getattr(P.prog, "direct_layers", ()) for g, _ in grp.gates)
+                if TAN_ROT and P.tan_ok and not direct and is_rotation(grp):
                     _emit_tan_rot(w, P, bits[0], "g_", nv if mode_bwd else 1, mode_bwd, classes)
                     if P.tan_count >= TAN_RENORM:
                         _renorm_rho(w, P, nv if mode_bwd else 1)
-                elif (EULER_TAN and general and P.drop_phase and P.walsh_diag
-                      and (cmag is not None or (P.tan_ok and EULER_BRANCH))):
+                elif (EULER_TAN and general and not direct and P.drop_phase and P.walsh_diag
+                        and (cmag is not None or (P.tan_ok and EULER_BRANCH))):
                     _emit_euler_tan(w, P, bits[0], "g_", nv if mode_bwd else 1, mode_bwd, classes,
                                     branch=cmag is None)
                     if P.tan_count >= TAN_RENORM:

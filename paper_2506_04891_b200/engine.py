@@ -151,7 +151,7 @@ class Engine:
     """A circuit compiled for the device; the object behind the drop-in API."""
 
     def __init__(self, circuit, M: int | None = None, R: int | None = None, device=None, jit=None,
-                 isolate=(), prefix=None, fold=None, split=None):
+                 isolate=(), prefix=None, fold=None, split=None, direct=(), split_layers=()):
         self.device = torch.device(device if device is not None else "cuda")
         if self.device.type != "cuda":
             raise ValueError("the engine runs on CUDA devices only")
@@ -177,7 +177,7 @@ class Engine:
         if split is None:
             split = os.environ.get("LSQ_SPLIT", "1") != "0"
         self.program = compile_circuit(circuit, M=M, R=R, isolate=isolate, prefix=prefix, fold=fold,
-                                       split=split)
+                                       split=split, direct=direct, split_layers=split_layers)
         self.prefix = bool(self.program.prefix) or bool(self.program.obs)
         self.native = NativeProgram(self.program, self.device)
         self.native.attach_jit()
@@ -517,7 +517,8 @@ _CACHE: "OrderedDict" = None
 _CACHE_MAX = 8  # engines (programs + held state buffers) kept alive, least recently used evicted
 
 
-def engine_for(circuit, device=None, M=None, R=None, jit=None, isolate=(), prefix=None) -> Engine:
+def engine_for(circuit, device=None, M=None, R=None, jit=None, isolate=(), prefix=None, direct=(),
+               split_layers=()) -> Engine:
     """Cached Engine per (circuit layers, n, tiling, variant, device)."""
     dev = torch.device(device if device is not None else "cuda")
     if dev.type == "cuda" and dev.index is None:
@@ -528,10 +529,13 @@ def engine_for(circuit, device=None, M=None, R=None, jit=None, isolate=(), prefi
 
         _CACHE = OrderedDict()
     isolate = tuple(sorted(set(int(i) for i in isolate)))
-    key = (_circuit_key(circuit), M, R, jit, isolate, prefix, str(dev))
+    direct = tuple(sorted(set(int(i) for i in direct)))
+    split_layers = tuple(sorted(set(int(i) for i in split_layers)))
+    key = (_circuit_key(circuit), M, R, jit, isolate, prefix, direct, split_layers, str(dev))
     eng = _CACHE.get(key)
     if eng is None:
-        eng = Engine(circuit, M=M, R=R, device=dev, jit=jit, isolate=isolate, prefix=prefix)
+        eng = Engine(circuit, M=M, R=R, device=dev, jit=jit, isolate=isolate, prefix=prefix, direct=direct,
+                     split_layers=split_layers)
         _CACHE[key] = eng
         while len(_CACHE) > _CACHE_MAX:
             _CACHE.popitem(last=False)

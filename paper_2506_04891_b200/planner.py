@@ -1,11 +1,20 @@
 """Per-layer method choice over CUDA variants (drop-in for reference planner.py:1-309).
 
 The reference times its nine CPU techniques per layer signature and replays the argmin
-(`build_plan`, planner.py:165-220). Here the candidates are CUDA execution variants of the
-same fused engine:
+(`build_plan`, planner.py:165-220). Here the candidates are CUDA implementations of the same
+fused engine, chosen per layer signature by measurement:
 
-* per layer: FUSED (the layer's gates join the surrounding tile passes) or ISOLATED (the
-  layer gets pass boundaries of its own -- the GPU analogue of one-layer-at-a-time);
+* FUSED    -- the default: the layer's gates join the surrounding fused groups and tile passes,
+              one-qubit groups in the Euler tangent form (6 packed ops per pair) where it
+              applies, diagonal parts split off by the codegen cost model;
+* ISOLATED -- the layer gets pass boundaries of its own (the GPU analogue of one layer at a
+              time): fewer fused gates per pass, lighter kernels;
+* DIRECT   -- (one-qubit non-diagonal gates) groups containing the layer's gates use the
+              direct complex 2x2 form (8 packed ops per pair, no run-time scale, no tangent
+              rotation);
+* SPLIT    -- (one-qubit diagonal gates) groups containing the layer's gates are split into a
+              diagonal run (phase table / sincos over many wires at once) and the non-diagonal
+              remainder, whatever the cost model says;
 * per circuit: the tile exponent M (bits per tile pass), part of the plan.
 
 Timing follows the reference protocol (warmup untimed, `reps` timed, mean and population
@@ -36,6 +45,8 @@ class KernelKind(Enum):
 
     FUSED = "fused"
     ISOLATED = "isolated"
+    DIRECT = "direct"
+    SPLIT = "split"
 
 
 KERNEL_ORDER = tuple(KernelKind)
@@ -48,7 +59,13 @@ def kernel_rank(kind: KernelKind) -> int:
 
 def applicable_variants(layer, n: int) -> tuple:
     positions(layer, n)  # validates the pattern
-    return KERNEL_ORDER
+    tr = gate_traits(layer.gate)
+    out = [KernelKind.FUSED, KernelKind.ISOLATED]
+    if tr.arity == 1 and not tr.diagonal and not tr.permutation:
+        out.append(KernelKind.DIRECT)
+    if tr.arity == 1 and tr.diagonal:
+        out.append(KernelKind.SPLIT)
+    return tuple(out)
 
 
 def default_variant(layer, n: int) -> KernelKind:
@@ -114,7 +131,8 @@ def _draw(circuit, batch, seed):
 
 
 def time_program(circuit, batch: int, objective: "Objective" = None, M=None, isolate=(), reps: int = 10,
-                 warmup: int = 3, timer=None, seed: int = 0, device=None) -> TimingStats:
+                 warmup: int = 3, timer=None, seed: int = 0, device=None, direct=(),
+                 split_layers=()) -> TimingStats:
     """Time the whole compiled program (one CUDA variant) with the reference's protocol:
     `warmup` untimed runs then `reps` timed runs (reference planner.py:106-162). Default clock:
     CUDA events on the engine's stream; an injected `timer` is called around each rep after
@@ -128,7 +146,7 @@ def time_program(circuit, batch: int, objective: "Objective" = None, M=None, iso
         raise ValueError("reps must be at least 1")
     if warmup < 0:
         raise ValueError("warmup cannot be negative")
-    eng = Engine(circuit, M=M, isolate=isolate, device=device,
+    eng = Engine(circuit, M=M, isolate=isolate, device=device, direct=direct, split_layers=split_layers,
                  fold=False if objective is Objective.FORWARD else None)
     th, x = _draw(circuit, batch, seed)
     th_d = None if th is None else torch.as_tensor(th, device=eng.device)
@@ -166,8 +184,9 @@ def build_plan(circuit, batch: int, objective: "Objective" = None, timer=None, r
     """Per-layer CUDA variant choice by measurement (reference build_plan, planner.py:165-220).
 
     1. tile exponent M: every candidate (<= n) is timed on the whole program; argmin.
-    2. per layer signature, in order of first appearance: ISOLATED is kept for all layers of the
-       signature iff it measures faster than the current assignment (ties -> FUSED, enum order).
+    2. per layer signature, in order of first appearance: every applicable variant (ISOLATED,
+       DIRECT, SPLIT) is timed on the whole program with the variants kept so far; the fastest
+       is kept for all layers of the signature (ties -> declaration order, FUSED first).
 
     `measure(layer, kernel) -> TimingStats` replaces real timing (tests): it is asked for the
     per-layer variants, and `measure(None, M)` for tile exponents.
@@ -176,18 +195,20 @@ def build_plan(circuit, batch: int, objective: "Objective" = None, timer=None, r
     n = int(circuit.n)
     layers = list(circuit.layers)
 
-    def timed(M, iso):
-        return time_program(circuit, batch, objective, M=M, isolate=iso, reps=reps, warmup=warmup,
-                            timer=timer, seed=seed)
+    def timed(M, assign):
+        sel = lambda kk: sorted(i for i, k in assign.items() if k is kk)  # noqa: E731
+        return time_program(circuit, batch, objective, M=M, isolate=sel(KernelKind.ISOLATED), reps=reps,
+                            warmup=warmup, timer=timer, seed=seed, direct=sel(KernelKind.DIRECT),
+                            split_layers=sel(KernelKind.SPLIT))
 
     if tile_bits is None:
         cands = sorted({min(n, m) for m in TILE_BITS_CANDIDATES})
-        stats_m = {m: (measure(None, m) if measure is not None else timed(m, ())) for m in cands}
+        stats_m = {m: (measure(None, m) if measure is not None else timed(m, {})) for m in cands}
         tile_bits = min(cands, key=lambda m: (stats_m[m].mean_seconds, -m))
         base = stats_m[tile_bits]
     else:
-        base = measure(None, tile_bits) if measure is not None else timed(tile_bits, ())
-    iso: set = set()
+        base = measure(None, tile_bits) if measure is not None else timed(tile_bits, {})
+    chosen: dict = {}  # layer index -> non-default variant kept so far
     cache: dict = {}
     measurements = []
     assignments = [KernelKind.FUSED] * len(layers)
@@ -196,17 +217,18 @@ def build_plan(circuit, batch: int, objective: "Objective" = None, timer=None, r
         if sig not in cache:
             members = [i for i, l in enumerate(layers) if layer_signature(l, n) == sig]
             stats = {}
-            if measure is not None:
-                for k in applicable_variants(layer, n):
+            for k in applicable_variants(layer, n):
+                if measure is not None:
                     stats[k] = measure(layer, k)
-            else:
-                stats[KernelKind.FUSED] = base
-                stats[KernelKind.ISOLATED] = timed(tile_bits, sorted(iso | set(members)))
+                elif k is KernelKind.FUSED:
+                    stats[k] = base
+                else:
+                    stats[k] = timed(tile_bits, {**chosen, **{i: k for i in members}})
             best = min(stats, key=lambda k: (stats[k].mean_seconds, kernel_rank(k)))
-            if best is KernelKind.ISOLATED:
-                iso |= set(members)
+            if best is not KernelKind.FUSED:
+                chosen.update({i: best for i in members})
                 if measure is None:
-                    base = stats[KernelKind.ISOLATED]
+                    base = stats[best]
             cache[sig] = (best, stats)
         best, stats = cache[sig]
         assignments[idx] = best

@@ -277,11 +277,13 @@ def _apply_cost(grp: Group, drop_phase: bool = False) -> int:
     return sum({"0": 0, "r": 1, "i": 1, "c": 2}[c] for row in cls for c in row)
 
 
-def split_diagonal(groups: list[Group], keep=(), drop_phase: bool = False) -> list[Group]:
+def split_diagonal(groups: list[Group], keep=(), drop_phase: bool = False, force=()) -> list[Group]:
     """Split one-qubit groups into runs of diagonal and non-diagonal gates when the
     non-diagonal remainder is cheaper to apply (RZ.RY -> real RY + a phase in a diagonal
     run). The diagonal parts then join diagonal runs, where a wire that is not a register bit
-    costs no per-amplitude work. Groups in `keep` (product-state prefix) stay whole."""
+    costs no per-amplitude work. Groups in `keep` (product-state prefix) stay whole; groups
+    with a gate of a layer in `force` (planner variant SPLIT) are split whatever the cost."""
+    force = set(force)
     out: list[Group] = []
     for g in groups:
         runs = []
@@ -294,7 +296,8 @@ def split_diagonal(groups: list[Group], keep=(), drop_phase: bool = False) -> li
         # a diagonal part followed by a non-diagonal one runs where its wire is a register bit
         # (one complex phase per amplitude, charged 4); trailing diagonal parts are deferred
         split = g.gid not in keep and g.arity == 1 and len(parts) > 1
-        if split and _os.environ.get("LSQ_SPLIT_FORCE") != "1":
+        forced = any(gr.layer in force for gr, _ in g.gates)
+        if split and not forced and _os.environ.get("LSQ_SPLIT_FORCE") != "1":
             cost = sum(_apply_cost(Group(0, g.wires, p), drop_phase) if not p[0][0].diag else
                        (4 if k < len(parts) - 1 else 0) for k, p in enumerate(parts))
             split = cost < _apply_cost(g, drop_phase)
@@ -646,11 +649,15 @@ def observable_masks(perms, n: int):
 
 
 def compile_circuit(circuit, M: int | None = None, R: int | None = None, isolate=(),
-                    prefix: bool = False, fold: bool = False, split: bool = False) -> Program:
+                    prefix: bool = False, fold: bool = False, split: bool = False, direct=(),
+                    split_layers=()) -> Program:
     """Compile a (reference-compatible) circuit into a pass program.
 
-    `isolate`: layer indices executed with pass boundaries of their own (planner variant
-    ISOLATED): their gates fuse only among themselves and share no pass with other layers.
+    Planner variants (layer indices): `isolate` -- executed with pass boundaries of their own
+    (ISOLATED): their gates fuse only among themselves and share no pass with other layers;
+    `direct` -- one-qubit groups containing a gate of these layers are applied in the direct
+    8-op form, not the Euler tangent form (DIRECT); `split_layers` -- one-qubit groups with a
+    gate of these (diagonal) layers are split into diagonal runs and the rest (SPLIT).
     """
     n = int(circuit.n)
     gates = flatten_gates(circuit)
@@ -676,7 +683,7 @@ def compile_circuit(circuit, M: int | None = None, R: int | None = None, isolate
         grp = fuse_groups(seg)
         if split:
             grp = split_diagonal(grp, set(prefix_groups(grp).values()) if (prefix and si == 0) else (),
-                                 drop_phase=fold)
+                                 drop_phase=fold, force=split_layers)
         preds = group_preds(grp)
         skip = set()
         if prefix and si == 0:
@@ -726,6 +733,8 @@ def compile_circuit(circuit, M: int | None = None, R: int | None = None, isolate
         T, E = c2.trainable_count, c2.encoding_count
     prog = Program(n, groups, passes, T, E, slot_base, total, M=M, gates=gates)
     prog.isolate = tuple(sorted(iso))
+    prog.direct_layers = frozenset(int(i) for i in direct)
+    prog.split_layers = tuple(sorted(int(i) for i in split_layers))
     prog.prefix = {w: gid for w, gid in pre.items()}
     prog.obs = obs
     prog.drop_phase = bool(fold)  # gradient program: global phases of constant groups dropped

@@ -364,6 +364,26 @@ def test_build_plan_real_timing_and_replay():
     assert_grads_close(a.grads, b.grads)
 
 
+@pytest.mark.parametrize("cfg,n", [(4, 12), (3, 12), (5, 12), (2, 12)])
+def test_all_variants_forced_vs_oracle(cfg, n):
+    """Every non-default per-layer variant at once (DIRECT on every one-qubit non-diagonal layer,
+    SPLIT on every diagonal one, ISOLATED on the entanglers of the first block) against the
+    oracle, so a plan may pick any of them."""
+    from paper_2506_04891_b200 import planner as P
+
+    wl = make_workload(cfg, n=n, batch=3)
+    K = P.KernelKind
+    assign = []
+    for i, layer in enumerate(wl.circuit.layers):
+        av = P.applicable_variants(layer, n)
+        assign.append(K.DIRECT if K.DIRECT in av else K.SPLIT if K.SPLIT in av else
+                      K.ISOLATED if i < 6 else K.FUSED)
+    plan = P.Plan(P.machine_id(), n, 3, P.Objective.FORWARD_BACKWARD, tuple(assign), (), 9)
+    res = gradient(wl.circuit, wl.theta, wl.x, batch=3, weights=wl.weights, plan=plan)
+    ref = orc.gradient(wl.circuit, wl.theta, wl.x, batch=3, weights=wl.weights)
+    check(res, ref, what=f"cfg{cfg}_all_variants")
+
+
 def test_choose_tile_bits_and_plan_replay():
     """Measured tile exponent (bench default) replayed through the public gradient()."""
     from paper_2506_04891_b200 import planner as P

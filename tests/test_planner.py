@@ -35,8 +35,41 @@ def test_build_plan_argmin_and_tile_bits():
     assert plan.tile_bits == 12
     for layer, k in zip(c.layers, plan.assignments):
         assert k is (P.KernelKind.ISOLATED if layer.gate is GateKind.RZZ else P.KernelKind.FUSED)
-    # every layer has a measurement for every variant
-    assert len(plan.measurements) == 2 * len(c.layers)
+    # every layer has a measurement for every applicable variant
+    assert len(plan.measurements) == sum(len(P.applicable_variants(l, c.n)) for l in c.layers)
+
+
+def test_variant_space_per_gate_kind():
+    """FUSED/ISOLATED everywhere, DIRECT for one-qubit non-diagonal gates (Euler/tangent form
+    off), SPLIT for one-qubit diagonal gates (forced diagonal runs)."""
+    K = P.KernelKind
+    n = 4
+    av = lambda g, pat=None: P.applicable_variants(Layer(g, pat or all_qubits(), Role.TRAINABLE  # noqa: E731
+                                                         if P.gate_traits(g).param_count else None), n)
+    assert av(GateKind.RY) == (K.FUSED, K.ISOLATED, K.DIRECT)
+    assert av(GateKind.RZ) == (K.FUSED, K.ISOLATED, K.SPLIT)
+    assert av(GateKind.CNOT, ring_pairs()) == (K.FUSED, K.ISOLATED)
+    assert av(GateKind.X) == (K.FUSED, K.ISOLATED)
+
+
+def test_variants_change_the_program():
+    """SPLIT forces the diagonal split of the groups it touches; DIRECT is recorded for the
+    codegen (both compile to valid programs the emulator runs like the default)."""
+    from emulator import Emulator
+    from oracle import layersim_oracle as orc
+    from paper_2506_04891_b200.configs import make_workload
+    from paper_2506_04891_b200.schedule import compile_circuit
+
+    wl = make_workload(4, n=6, batch=2)
+    rz = [i for i, l in enumerate(wl.circuit.layers) if l.gate is GateKind.RZ and l.role is Role.TRAINABLE]
+    sx = [i for i, l in enumerate(wl.circuit.layers) if l.gate is GateKind.SX]
+    base = compile_circuit(wl.circuit, M=4, R=2, split=True)
+    forced = compile_circuit(wl.circuit, M=4, R=2, split=True, split_layers=rz, direct=sx)
+    assert len(forced.groups) > len(base.groups)
+    assert forced.direct_layers == frozenset(sx)
+    ref = orc.gradient(wl.circuit, wl.theta, wl.x, batch=2, weights=wl.weights)
+    res = Emulator(forced).gradient(wl.theta, wl.x, 2, wl.weights)
+    np.testing.assert_allclose(res["grads"], ref["grads"], atol=1e-9)
 
 
 def test_tie_break_prefers_declaration_order():
