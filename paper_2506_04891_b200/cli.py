@@ -72,6 +72,16 @@ def load_params(path):
     return tr, en
 
 
+def _parse_qubits(text: str) -> tuple:
+    """'5' -> (5,); '4..7' -> (4, 5, 6, 7); '4,6,8' -> (4, 6, 8) (reference cli.py:30-38)."""
+    if ".." in text:
+        lo, hi = (int(v) for v in text.split("..", 1))
+        if hi < lo:
+            raise ValueError(f"empty qubit range {text!r}")
+        return tuple(range(lo, hi + 1))
+    return tuple(int(part) for part in text.split(","))
+
+
 def _build_parser():
     p = argparse.ArgumentParser(prog="paper_2506_04891_b200",
                                 description="B200 layer-wise state-vector engine")
@@ -90,6 +100,18 @@ def _build_parser():
     s.add_argument("--warmup", type=int, default=3)
     s.add_argument("--seed", type=int, default=0)
     s.add_argument("--out", required=True)
+    s = sub.add_parser("bench", help="timing sweep over a circuit family on the GPU, CSV reports")
+    s.add_argument("--family", required=True, choices=("vq", "qdi", "ibm", "ionq"))
+    s.add_argument("--qubits", required=True, type=_parse_qubits, metavar="A..B|N[,M...]")
+    s.add_argument("--batch", default=(1,), type=lambda t: tuple(int(x) for x in t.split(",")),
+                   metavar="B[,B2...]")
+    s.add_argument("--blocks", type=int, default=8)
+    s.add_argument("--reps", type=int, default=10)
+    s.add_argument("--warmup", type=int, default=3)
+    s.add_argument("--objective", choices=["forward", "forward+backward"], default="forward")
+    s.add_argument("--seed", type=int, default=0)
+    s.add_argument("--out", required=True)
+    s.add_argument("--plan", default=None, help="replay a saved plan file")
     s = sub.add_parser("compile", help="compile a circuit into a program artifact for lsq_program_load")
     g = s.add_mutually_exclusive_group(required=True)
     g.add_argument("--circuit", help="reference circuit JSON file")
@@ -143,6 +165,19 @@ def _cmd_plan(args) -> int:
     return 0
 
 
+def _cmd_bench(args) -> int:
+    from .harness import BenchConfig, crossover_path, run_benchmark
+    from .planner import Objective
+
+    config = BenchConfig(family=args.family, qubits=tuple(args.qubits), batches=tuple(args.batch),
+                         blocks=args.blocks, reps=args.reps, warmup=args.warmup,
+                         objective=Objective(args.objective), seed=args.seed, out=args.out, plan_path=args.plan)
+    rows = run_benchmark(config)
+    print(f"wrote {len(rows)} rows to {args.out}")
+    print(f"wrote kernel choices to {crossover_path(args.out)}")
+    return 0
+
+
 def _cmd_compile(args) -> int:
     """Host-only (no GPU): circuit -> schedule -> generated kernels -> one artifact file."""
     from . import artifact
@@ -169,7 +204,8 @@ def _cmd_compile(args) -> int:
     return 0
 
 
-_COMMANDS = {"run": _cmd_run, "grad": _cmd_grad, "plan": _cmd_plan, "compile": _cmd_compile}
+_COMMANDS = {"run": _cmd_run, "grad": _cmd_grad, "plan": _cmd_plan, "compile": _cmd_compile,
+             "bench": _cmd_bench}
 
 
 def main(argv=None) -> int:

@@ -419,6 +419,62 @@ def schedule_passes(groups, n, M, seeds: int = 12, skip=()) -> list[PassPlan]:
     return passes
 
 
+def _fp_cost(g: Group) -> float:
+    """Estimated packed-FP32 ops per amplitude of one group in an adjoint kernel (U^+ on psi and
+    lambda plus couplings); forward kernels are about half. Diagonal groups ride on runs."""
+    if g.diag:
+        return 1.0
+    if g.arity == 1:
+        return 11.0 if g.needs_grad else 6.0
+    return 8.0 if any(GATE_TRAITS[x.kind].param_count for x, _ in g.gates) else 3.0
+
+
+# adjoint-pass budget in packed ops per amplitude that still hides under its HBM time (3
+# vector transfers, 24 B per amplitude, at ~70% of the FP32 and HBM peaks)
+REBALANCE_BUDGET = float(_os.environ.get("LSQ_REBALANCE_BUDGET", "40"))
+REBALANCE = _os.environ.get("LSQ_REBALANCE", "1") != "0"
+
+
+def rebalance_passes(passes: list[PassPlan], groups, n: int) -> None:
+    """Move work from heavy passes into the light ones after them (in place). The greedy
+    partition packs each pass as full as its tile allows, so the last passes of a circuit carry
+    little FP32 work and run at the HBM roofline with the FMA pipe mostly idle (cfg4's last two
+    adjoint passes: 15% FMA-pipe activity). Walking from the last pass back, a pass whose
+    estimated FP32 load is under REBALANCE_BUDGET takes groups from the end of the pass before
+    it: a group may move when every group that depends on it is already in a later pass and,
+    if it is not diagonal, its wires are tile wires of the receiving pass. Program semantics are
+    unchanged (dependencies stay ordered; gids are a topological order)."""
+    if len(passes) < 2:
+        return
+    succ = [set() for _ in groups]
+    for g in groups:
+        for p_ in group_preds(groups)[g.gid]:
+            succ[p_].add(g.gid)
+    where = {gid: i for i, pp in enumerate(passes) for gid in pp.groups}
+    for i in range(len(passes) - 1, 0, -1):
+        dst, src = passes[i], passes[i - 1]
+        load = sum(_fp_cost(groups[x]) for x in dst.groups)
+        moved = True
+        while moved and load < REBALANCE_BUDGET:
+            moved = False
+            for gid in sorted(src.groups, reverse=True):
+                g = groups[gid]
+                if any(where.get(sx, -1) <= i - 1 for sx in succ[gid]):
+                    continue  # a dependent group stays in this pass or earlier
+                if not g.diag and not set(g.wires) <= dst.tile_wires:
+                    continue
+                c = _fp_cost(g)
+                if load + c > REBALANCE_BUDGET:
+                    continue
+                src.groups.remove(gid)
+                dst.groups = sorted(dst.groups + [gid])
+                where[gid] = i
+                load += c
+                moved = True
+                break
+    passes[:] = [pp for pp in passes if pp.groups] or passes[:1]
+
+
 # ----------------------------------------------------------------------------- phases
 
 # Shared-memory XOR swizzle of the amplitude index: S(L) = L ^ h(L >> 4), h linear into local
@@ -697,6 +753,8 @@ def compile_circuit(circuit, M: int | None = None, R: int | None = None, isolate
             for gid in tr:
                 grp[gid].trailing = True
         seg_passes = schedule_passes(grp, n, M, skip=skip) if (grp or not passes) else []
+        if REBALANCE and not (prefix and si == 0 and len(segs) > 1):
+            rebalance_passes(seg_passes, grp, n)
         need2 = any(g.arity == 2 and not g.diag for g in grp)
         for pp in seg_passes:
             r = default_r(pp.M) if R is None else min(R, pp.M)

@@ -66,3 +66,40 @@ def test_cli_run_and_grad_match_oracle(tmp_path, capsys):
     out = json.loads(capsys.readouterr().out)
     np.testing.assert_allclose(out["value"], ref["value"], atol=1e-5)
     np.testing.assert_allclose(out["grads"], ref["grads"], atol=1e-4)
+
+
+def test_bench_families_and_qubit_parser():
+    """The harness's circuit families and argument parsing (reference bench.py:81-136,
+    cli.py:30-38), checked on CPU against the oracle through the emulator."""
+    from emulator import Emulator
+    from paper_2506_04891_b200 import harness
+    from paper_2506_04891_b200.schedule import compile_circuit
+
+    assert cli._parse_qubits("4..6") == (4, 5, 6) and cli._parse_qubits("4,8") == (4, 8)
+    with pytest.raises(ValueError):
+        cli._parse_qubits("6..4")
+    with pytest.raises(ValueError):
+        harness.BenchConfig("nope", (4,), (1,))
+    for fam in harness.FAMILIES:
+        c = harness.build_circuit(fam, 5, 2)
+        tr, en = harness.draw_params(c, 3, 0, 5)
+        res = Emulator(compile_circuit(c, M=4, R=2)).gradient(tr, en, 3, None)
+        ref = orc.gradient(c, tr, en, batch=3)
+        np.testing.assert_allclose(res["grads"], ref["grads"], atol=1e-9)
+
+
+@pytest.mark.gpu
+def test_bench_subcommand_writes_reports(tmp_path):
+    pytest.importorskip("torch").cuda.is_available() or pytest.skip("needs a GPU")
+    out = tmp_path / "r.csv"
+    rc = cli.main(["bench", "--family", "ibm", "--qubits", "6,8", "--batch", "4", "--blocks", "2",
+                   "--reps", "2", "--warmup", "1", "--objective", "forward+backward", "--out", str(out)])
+    assert rc == 0
+    import csv
+
+    rows = list(csv.reader(open(out)))
+    assert tuple(rows[0])[:10] == ("family", "n", "batch", "phase", "plan_source", "mean_s", "std_s", "reps",
+                                   "warmup", "seed")
+    assert len(rows) == 1 + 2 * 3 and {r[3] for r in rows[1:]} == {"forward", "backward", "total"}
+    cross = list(csv.reader(open(tmp_path / "r_crossover.csv")))
+    assert cross[0] == ["family", "n", "batch", "gate", "pattern", "role", "kernel"] and len(cross) > 1
