@@ -1099,16 +1099,42 @@ def _sx_open(w, k, P=None):
     return f"sx{k}"
 
 
+# swizzled shared index S(tp | loc) = (S(tp) ^ lo) + hi with lo = S(loc) & 0xE (the swizzle bits)
+# and hi = the rest: the thread and register parts are disjoint local bits and the swizzle only
+# writes bits 1..3, so after XOR-ing the (at most 8) distinct lo values into per-transpose bases
+# every access is base + immediate (LDS/STS [R + imm]) instead of one LOP3 per access
+SWZ_IMM = os.environ.get("LSQ_SWZ_IMM", "1") != "0"
+
+
+def _swz_index(w, P, sx, offs, buf):
+    """(pointer, index) expressions of the swizzled offsets `offs` off the thread base `sx` in
+    `buf`: with SWZ_IMM one shared pointer per distinct swizzle-bit value and a constant index
+    (folded into the LDS/STS immediate), else the buffer and an XOR-ed index."""
+    if not SWZ_IMM:
+        return [(buf, f"{sx} ^ {o}u") for o in offs]
+    names = {}
+    out = []
+    for o in offs:
+        lo, hi = o & 0xE, o & ~0xE
+        if lo not in names:
+            names[lo] = f"{sx}p{lo}_"
+            w(f"float2* const {names[lo]} = {buf} + ({sx} ^ {lo}u);")
+        out.append((names[lo], f"{hi}u"))
+    return out
+
+
 def _emit_put(w, P, buf, a, q):
     """vector q (registers, layout a) -> buf (swizzled)"""
     pr = _pairs(P, a)
     sx = _sx_open(w, a, P)
     if pr is None:
+        idx = _swz_index(w, P, sx, [P.soff(a, i) for i in range(P.NR)], buf)
         for i in range(P.NR):
-            w(f"{buf}[{sx} ^ {P.soff(a, i)}u] = v[{q}][{i}];")
+            w(f"{idx[i][0]}[{idx[i][1]}] = v[{q}][{i}];")
     else:
-        for i, j in pr:
-            w(f"st_pair({buf}, {sx} ^ {P.soff(a, i)}u, v[{q}][{i}], v[{q}][{j}]);")
+        idx = _swz_index(w, P, sx, [P.soff(a, i) for i, _ in pr], buf)
+        for (i, j), (pb, e) in zip(pr, idx):
+            w(f"st_pair({pb}, {e}, v[{q}][{i}], v[{q}][{j}]);")
     w("}")
 
 
@@ -1117,11 +1143,13 @@ def _emit_get(w, P, buf, b, q):
     pr = _pairs(P, b)
     sx = _sx_open(w, b, P)
     if pr is None:
+        idx = _swz_index(w, P, sx, [P.soff(b, i) for i in range(P.NR)], buf)
         for i in range(P.NR):
-            w(f"v[{q}][{i}] = {buf}[{sx} ^ {P.soff(b, i)}u];")
+            w(f"v[{q}][{i}] = {idx[i][0]}[{idx[i][1]}];")
     else:
-        for i, j in pr:
-            w(f"ld_pair({buf}, {sx} ^ {P.soff(b, i)}u, v[{q}][{i}], v[{q}][{j}]);")
+        idx = _swz_index(w, P, sx, [P.soff(b, i) for i, _ in pr], buf)
+        for (i, j), (pb, e) in zip(pr, idx):
+            w(f"ld_pair({pb}, {e}, v[{q}][{i}], v[{q}][{j}]);")
     w("}")
 
 

@@ -11,7 +11,23 @@ cfg = int(a[0] or 2); steps = int(a[1] or 3)
 batch = int(a[2]) if a[2] not in (None, "0") else None
 M = int(a[3]) if a[3] else None; R = int(a[4]) if a[4] else None
 wl = make_workload(cfg, batch=batch)
-eng = Engine(wl.circuit, M=M, R=R)
+# the program bench.py times: its saved per-layer plan when one exists and no M is forced
+plan_path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "plans", f"cfg{cfg}.json")
+kw = {}
+if M is None and os.path.exists(plan_path):
+    import warnings
+
+    from paper_2506_04891_b200.core import plan_kernels
+    from paper_2506_04891_b200.planner import KernelKind, load_plan
+
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        plan = load_plan(plan_path)
+    kinds = plan_kernels(wl.circuit, plan)
+    sel = lambda kk: [i for i, k in enumerate(kinds) if k is kk]  # noqa: E731
+    M = plan.tile_bits
+    kw = dict(isolate=sel(KernelKind.ISOLATED), direct=sel(KernelKind.DIRECT), split_layers=sel(KernelKind.SPLIT))
+eng = Engine(wl.circuit, M=M, R=R, **kw)
 th = torch.as_tensor(wl.theta, device="cuda"); x = torch.as_tensor(wl.x, device="cuda")
 w = torch.as_tensor(wl.weights, device="cuda")
 bufs = None

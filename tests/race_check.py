@@ -34,10 +34,18 @@ def parse_blocks(body: str) -> Node:
     as a whole '}' line, or a whole one-line block `{ ... }`)."""
     root = Node()
     stack = [root]
+    alias = {}  # shared pointers off a buffer (codegen SWZ_IMM): name -> buffer expression
     for raw in body.splitlines():
         line = raw.strip()
         if not line:
             continue
+        m = re.search(r"float2\* const (\w+) = (\(s_stage \+ \d+\)|s_x|s_stage) \+", line)
+        if m:  # a (re)definition: no accesses on this line
+            alias[m.group(1)] = m.group(2)
+            continue
+        for name, bexpr in alias.items():
+            if name in line:
+                line = re.sub(r"\b" + re.escape(name) + r"\b", bexpr, line)
         opens, closes = line.count("{"), line.count("}")
         if line.startswith("}") and "else" in line and line.endswith("{"):  # "} else {"
             if len(stack) > 1:
