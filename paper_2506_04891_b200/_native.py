@@ -28,7 +28,7 @@ _SIGS = {
     "lsq_device_info": (_I, [_I, _c.c_char_p, _I]),
     "lsq_program_create": (_I, [_P, _I64, _P, _I64, _c.POINTER(_P)]),
     "lsq_program_destroy": (None, [_P]),
-    "lsq_program_jit": (_I, [_P, _I, _P, _P, _P, _P, _P, _c.c_char_p, _I]),
+    "lsq_program_jit": (_I, [_P, _I, _P, _P, _P, _P, _P, _P, _c.c_char_p, _I]),
     "lsq_program_info": (_I, [_P, _P]),
     "lsq_program_load": (_I, [_c.c_char_p, _c.c_char_p, _c.POINTER(_P)]),
     "lsq_workspace_bytes": (_I64, [_P, _I]),

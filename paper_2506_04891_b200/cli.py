@@ -196,10 +196,12 @@ def _cmd_compile(args) -> int:
         m = min(circuit.n, M if M is not None else DEFAULT_M)
         R = DEFAULT_R_SPECIALISED if m >= 9 else default_r(m)
     sel = lambda kk: [] if plan is None else [i for i, k in enumerate(plan.assignments) if k is kk]  # noqa: E731
-    prog = compile_circuit(circuit, M=M, R=R, isolate=sel(KernelKind.ISOLATED), prefix=args.gradient,
-                           fold=args.gradient, split=True, direct=sel(KernelKind.DIRECT),
-                           split_layers=sel(KernelKind.SPLIT))
-    size = artifact.write(prog, args.out)
+    from .engine import forward_program
+
+    kw = dict(isolate=sel(KernelKind.ISOLATED), prefix=args.gradient, fold=args.gradient, split=True,
+              direct=sel(KernelKind.DIRECT), split_layers=sel(KernelKind.SPLIT))
+    prog = compile_circuit(circuit, M=M, R=R, **kw)
+    size = artifact.write(prog, args.out, forward_program(circuit, prog, M=M, **kw))
     print(f"wrote {args.out}: n={circuit.n}, {len(prog.passes)} passes, {size} bytes")
     return 0
 

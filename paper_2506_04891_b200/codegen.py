@@ -1258,7 +1258,11 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
             rot = _Rot(P, 1)
     est_regs = 2 * P.NR * nv + 40
     minb = max(1, min(4, 65536 // (P.NT * est_regs)))
-    if mode == MODE_FWD:
+    if mode == MODE_FWD and P.R >= 5:
+        # forward kernels with 32 amplitudes per thread: 128 registers (64 data), 4 CTAs of 128
+        # threads per SM (LSQ_MINB_FWD5 overrides, A/B runs)
+        minb = int(os.environ.get("LSQ_MINB_FWD5", "4"))
+    elif mode == MODE_FWD:
         # forward kernels: an 80-register budget (measured: 256-thread tiles at 3 CTAs/SM beat 2,
         # 128-thread tiles at 6 beat 4 -- occupancy wins over a few spills)
         minb = max(1, min(8, 65536 // (P.NT * 80)))
@@ -1914,6 +1918,16 @@ def generate_kernels(prog) -> list:
     for pi, mode in program_modes(prog):
         out.append((pi, mode, kernel_name(pi, mode), prims + "\n" + emit_kernel(prog, pi, mode) + "\n",
                     stage_vectors(prog, pi, mode)))
+    return out
+
+
+def kernel_set(prog, prog_fwd=None) -> list:
+    """[(pass, mode, name, source, stage_vecs, reg_bits)] of a program; with `prog_fwd` (the same
+    pass partition compiled with more register bits, see engine.forward_program) the forward
+    kernels come from it: 2^R_fwd amplitudes per thread and fewer phase transposes."""
+    out = [k + (prog.passes[k[0]].R,) for k in generate_kernels(prog) if prog_fwd is None or k[1] != MODE_FWD]
+    if prog_fwd is not None:
+        out += [k + (prog_fwd.passes[k[0]].R,) for k in generate_kernels(prog_fwd) if k[1] == MODE_FWD]
     return out
 
 

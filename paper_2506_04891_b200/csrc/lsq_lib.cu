@@ -749,7 +749,7 @@ int jit_compile(const std::string& src, const std::string& cache_dir, std::strin
 }  // namespace
 
 int lsq_program_jit(lsq_program* P, int nk, const char* const* sources, const int* pass_idx,
-                    const int* modes, const int* stage_vecs, const char* const* names,
+                    const int* modes, const int* stage_vecs, const int* reg_bits, const char* const* names,
                     const char* cache_dir, int threads) {
   if (!P || nk < 0 || (nk && (!sources || !pass_idx || !modes || !names)))
     return fail(LSQ_EINVAL, "bad JIT arguments");
@@ -779,7 +779,11 @@ int lsq_program_jit(lsq_program* P, int nk, const char* const* sources, const in
     JitKernel& jk = P->jit[pass_idx[i] * 3 + modes[i]];
     jk.fn = (const void*)kern;
     const PassInfo& pi = P->passes[pass_idx[i]];
-    jk.NT = 1 << (pi.M - pi.R);
+    // a kernel may tile its registers differently from the program's phase plan (forward kernels
+    // with 2^5 amplitudes per thread): reg_bits[i] sets its thread count
+    const int kr = reg_bits && reg_bits[i] > 0 ? reg_bits[i] : pi.R;
+    if (kr < 1 || kr > pi.M || kr > MAX_R) return fail(LSQ_EINVAL, "bad register bits for a JIT kernel");
+    jk.NT = 1 << (pi.M - kr);
     // specialised kernels may add a next-tile prefetch stage of stage_vecs[i] x 2^M amplitudes
     const int NV = modes[i] == 0 ? 1 : 2;
     const int sv = stage_vecs ? stage_vecs[i] : NV;
@@ -810,7 +814,8 @@ int lsq_program_load(const char* path, const char* cache_dir, lsq_program** out)
   int32_t nk = 0;
   if (!take(magic, 4) || memcmp(magic, "LSQP", 4) != 0) return fail(LSQ_EINVAL, "not a program artifact (magic)");
   if (!take(&version, 4)) return fail(LSQ_EINVAL, "truncated program artifact");
-  if (version != 1) return fail(LSQ_EPLAN, "program artifact version " + std::to_string(version) + " != 1");
+  if (version != 1 && version != 2)
+    return fail(LSQ_EPLAN, "program artifact version " + std::to_string(version) + " not in {1, 2}");
   if (!take(&nw, 8) || !take(&nf, 8) || !take(&nk, 4) || nw < HDR_WORDS || nf < 0 || nk < 0 ||
       (size_t)nw > blob.size() / 4 || (size_t)nf > blob.size() / 8)
     return fail(LSQ_EINVAL, "corrupt program artifact header");
@@ -819,12 +824,12 @@ int lsq_program_load(const char* path, const char* cache_dir, lsq_program** out)
   if (!take(words.data(), 4 * (size_t)nw) || !take(fvals.data(), 8 * (size_t)nf))
     return fail(LSQ_EINVAL, "truncated program artifact (words)");
   std::vector<std::string> srcs((size_t)nk), names((size_t)nk);
-  std::vector<int> pidx((size_t)nk), modes((size_t)nk), stages((size_t)nk);
+  std::vector<int> pidx((size_t)nk), modes((size_t)nk), stages((size_t)nk), regs((size_t)nk, 0);
   for (int i = 0; i < nk; ++i) {
     int32_t nl = 0;
     int64_t sl = 0;
-    if (!take(&pidx[i], 4) || !take(&modes[i], 4) || !take(&stages[i], 4) || !take(&nl, 4) || nl < 1 ||
-        (size_t)nl > blob.size() - off)
+    if (!take(&pidx[i], 4) || !take(&modes[i], 4) || !take(&stages[i], 4) || (version >= 2 && !take(&regs[i], 4)) ||
+        !take(&nl, 4) || nl < 1 || (size_t)nl > blob.size() - off)
       return fail(LSQ_EINVAL, "corrupt program artifact (kernel header)");
     names[i].resize((size_t)nl);
     if (!take(&names[i][0], (size_t)nl) || !take(&sl, 8) || sl < 1 || (size_t)sl > blob.size() - off)
@@ -841,7 +846,8 @@ int lsq_program_load(const char* path, const char* cache_dir, lsq_program** out)
     sp[i] = srcs[i].c_str();
     np[i] = names[i].c_str();
   }
-  rc = lsq_program_jit(P, nk, sp.data(), pidx.data(), modes.data(), stages.data(), np.data(), cache_dir, 0);
+  rc = lsq_program_jit(P, nk, sp.data(), pidx.data(), modes.data(), stages.data(), regs.data(), np.data(),
+                       cache_dir, 0);
   if (rc) {
     lsq_program_destroy(P);
     return rc;

@@ -77,17 +77,19 @@ class NativeProgram:
         self.profiling = False
         self.profile = []
 
-    def attach_jit(self, cache_dir=None):
-        """Compile the per-pass specialised kernels (codegen.py) with NVRTC for sm_100a."""
+    def attach_jit(self, cache_dir=None, prog_fwd=None):
+        """Compile the per-pass specialised kernels (codegen.py) with NVRTC for sm_100a; with
+        `prog_fwd` the forward kernels come from that register tiling (engine.forward_program)."""
         from . import codegen
 
-        ks = codegen.generate_kernels(self.prog)
+        ks = codegen.kernel_set(self.prog, prog_fwd)
         n = len(ks)
         srcs = (ctypes.c_char_p * n)(*[k[3].encode() for k in ks])
         names = (ctypes.c_char_p * n)(*[k[2].encode() for k in ks])
         pidx = (ctypes.c_int * n)(*[k[0] for k in ks])
         modes = (ctypes.c_int * n)(*[k[1] for k in ks])
         stages = (ctypes.c_int * n)(*[k[4] for k in ks])
+        regs = (ctypes.c_int * n)(*[k[5] for k in ks])
         if cache_dir is None:
             cache_dir = os.environ.get("LSQ_CACHE_DIR", os.path.join(os.path.expanduser("~"), ".cache", "lsq_jit"))
         if cache_dir:
@@ -97,7 +99,7 @@ class NativeProgram:
                 _native.lib().lsq_program_jit(
                     self.handle, n, ctypes.cast(srcs, ctypes.c_void_p), ctypes.cast(pidx, ctypes.c_void_p),
                     ctypes.cast(modes, ctypes.c_void_p), ctypes.cast(stages, ctypes.c_void_p),
-                    ctypes.cast(names, ctypes.c_void_p),
+                    ctypes.cast(regs, ctypes.c_void_p), ctypes.cast(names, ctypes.c_void_p),
                     cache_dir.encode() if cache_dir else None, 0,
                 )
             )
@@ -147,6 +149,29 @@ class NativeProgram:
         return int(_native.lib().lsq_last_launch_count(self.handle))
 
 
+def forward_register_bits(M: int) -> int | None:
+    """Register bits of the forward kernels when they differ from the program's (LSQ_R_FWD:
+    0 = same as the adjoint's): one vector per thread leaves room for 2^5 amplitudes, which
+    means fewer phase transposes; needs tiles of >= 2^10 amplitudes (>= 32 threads)."""
+    r = int(os.environ.get("LSQ_R_FWD", "5"))
+    return r if r > 0 and M - r >= 5 else None
+
+
+def forward_program(circuit, prog, M=None, **kw):
+    """The same pass partition compiled with the forward register tiling (or None): identical
+    groups and tile wires per pass -- only the phase plans differ -- so its forward kernels run
+    against the program's tables and checkpoints unchanged."""
+    if not prog.passes:
+        return None
+    rf = forward_register_bits(prog.passes[0].M)
+    if rf is None or rf == prog.passes[0].R or any(pp.M != prog.passes[0].M for pp in prog.passes):
+        return None
+    pf = compile_circuit(circuit, M=M, R=rf, **kw)
+    same = len(pf.passes) == len(prog.passes) and all(
+        a.groups == b.groups and a.tile_wires == b.tile_wires for a, b in zip(pf.passes, prog.passes))
+    return pf if same else None
+
+
 class Engine:
     """A circuit compiled for the device; the object behind the drop-in API."""
 
@@ -176,11 +201,12 @@ class Engine:
         # diagonal gates split out of one-qubit groups when the remainder is cheaper
         if split is None:
             split = os.environ.get("LSQ_SPLIT", "1") != "0"
-        self.program = compile_circuit(circuit, M=M, R=R, isolate=isolate, prefix=prefix, fold=fold,
-                                       split=split, direct=direct, split_layers=split_layers)
+        kw = dict(isolate=isolate, prefix=prefix, fold=fold, split=split, direct=direct, split_layers=split_layers)
+        self.program = compile_circuit(circuit, M=M, R=R, **kw)
+        self.program_fwd = forward_program(circuit, self.program, M=M, **kw)
         self.prefix = bool(self.program.prefix) or bool(self.program.obs)
         self.native = NativeProgram(self.program, self.device)
-        self.native.attach_jit()
+        self.native.attach_jit(prog_fwd=self.program_fwd)
         self.variant = "jit"
         self.T = self.program.trainable_count
         self.E = self.program.encoding_count

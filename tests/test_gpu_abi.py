@@ -57,7 +57,7 @@ def test_artifact_program_equals_engine(tmp_path):
     eng = Engine(wl.circuit, M=9)
     assert len(eng.program.passes) > 1
     path = tmp_path / "cfg2_n12.lsqp"
-    artifact.write(eng.program, str(path))
+    artifact.write(eng.program, str(path), eng.program_fwd)
     h = ctypes.c_void_p()
     _native.check(_native.lib().lsq_program_load(str(path).encode(), None, ctypes.byref(h)))
     try:

@@ -83,7 +83,7 @@ def test_program_artifact_roundtrip_and_loader_errors(tmp_path):
     d = artifact.decode(blob)
     assert list(d["words"]) == list(prog.words)
     assert len(d["kernels"]) == 2 * len(prog.passes)
-    assert all(src.count("__global__") >= 1 for _, _, _, src, _ in d["kernels"])
+    assert all(src.count("__global__") >= 1 for _, _, _, src, _, _ in d["kernels"])
     if not os.path.exists(_native.LIB_PATH):
         return
     lib = _native.load_library()
@@ -92,7 +92,7 @@ def test_program_artifact_roundtrip_and_loader_errors(tmp_path):
     bad.write_bytes(b"NOPE" + blob[4:])
     assert lib.lsq_program_load(str(bad).encode(), None, ctypes.byref(h)) == 1
     ver = tmp_path / "ver.lsqp"
-    ver.write_bytes(blob[:4] + (2).to_bytes(4, "little") + blob[8:])
+    ver.write_bytes(blob[:4] + (3).to_bytes(4, "little") + blob[8:])
     assert lib.lsq_program_load(str(ver).encode(), None, ctypes.byref(h)) == 2
     trunc = tmp_path / "trunc.lsqp"
     trunc.write_bytes(blob[: len(blob) // 2])

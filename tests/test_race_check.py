@@ -24,12 +24,22 @@ def _kernels(cfg, n, M, prefix=True):
     return prog, codegen.generate_kernels(prog)
 
 
+def _kernels_r(cfg, n, M, prefix, R):
+    wl = make_workload(cfg, n=n, batch=2)
+    prog = compile_circuit(wl.circuit, M=M, R=R, prefix=prefix, fold=prefix, split=True)
+    return prog, codegen.generate_kernels(prog)
+
+
 @pytest.mark.parametrize("cfg,n,M", CASES)
 def test_generated_kernels_race_free(cfg, n, M):
     for prefix in ((True, False) if n <= 16 else (True,)):
         prog, ks = _kernels(cfg, n, M, prefix)
+        if (M or n) >= 10:  # the forward kernels' 2^5-amplitude register tiling (engine.forward_program)
+            p5, k5 = _kernels_r(cfg, n, M, prefix, 5)
+            ks = ks + [k for k in k5 if k[1] == 0]
         for pi, mode, name, src, _ in ks:
-            hazards, npaths = check_kernel_source(src, name, prog.passes[pi].M)
+            pp = prog.passes[pi]
+            hazards, npaths = check_kernel_source(src, name, pp.M)
             assert npaths > 0
             assert not hazards, f"{name}: {hazards[:3]}"
 

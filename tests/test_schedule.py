@@ -45,6 +45,21 @@ def test_forward_state_matches_oracle():
     np.testing.assert_allclose(psi, ref, atol=1e-9)
 
 
+@pytest.mark.parametrize("cfg", [2, 4, 5])
+def test_forward_register_tiling_same_partition(cfg):
+    """The forward kernels' coarser register tiling (engine.forward_program, R=5) keeps the pass
+    partition -- groups and tile wires -- and its own phase plan computes the same states."""
+    from paper_2506_04891_b200.engine import forward_program
+
+    wl = make_workload(cfg, n=13, batch=2)
+    kw = dict(prefix=False, fold=False, split=True)
+    p4 = S.compile_circuit(wl.circuit, M=10, R=4, **kw)
+    p5 = forward_program(wl.circuit, p4, M=10, **kw)
+    assert p5 is not None and all(pp.R == 5 for pp in p5.passes)
+    psi = Emulator(p5).forward(wl.theta, wl.x, 2)
+    np.testing.assert_allclose(psi, orc.apply_circuit(wl.circuit, wl.theta, wl.x, batch=2), atol=1e-9)
+
+
 def test_cfg1_full_golden():
     gold = load_golden("cfg1_full")
     wl = make_workload(1)
