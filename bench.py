@@ -678,6 +678,7 @@ def run_ours(args, world, rank, local):
     # ---- roofline: per-launch CUDA events on the engine's stream (separate profiled steps)
     eng.native.set_profiling(True)
     per_kernel = {}
+    sol = []  # (speed-of-light seconds, measured seconds, flops known) per profiled pass launch
     nprof = max(2, min(args.steps, 5))
     # executed FP32 flops per row of each pass kernel, from ncu source counters of the same
     # kernels (profiles/ncu_fp32.py); the launch times below are this run's own CUDA events
@@ -703,6 +704,9 @@ def run_ours(args, world, rank, local):
                 d["flops"] = d.get("flops", 0.0) + fl * rows_launch
             else:
                 d["flops_missing"] = True
+            # per-launch speed of light: the larger of its FP32 and its HBM time at the peaks
+            sol.append((max((fl or 0.0) * rows_launch / (FP32_PEAK_TFLOPS * 1e12),
+                            vec * rows_launch * (8 << n) / (_peaks()[0] * 1e9)), t / 1e3, fl is not None))
     eng.native.set_profiling(False)
     peak, peak_src = _peaks()
     dom = max(per_kernel.items(), key=lambda kv: kv[1]["ms"])
@@ -725,6 +729,11 @@ def run_ours(args, world, rank, local):
                              "frac": round(all_b / (all_ms / 1e3) / 1e9 / peak, 4),
                              "share_of_step": round((all_ms / nprof) / (ms / args.steps), 4)},
         "fp32": _fp32_view(per_kernel, dom[0]),
+        # every pass launch bounded by whichever of FP32 and HBM it needs more time for
+        "speed_of_light": ({"frac": round(sum(a for a, _, _ in sol) / sum(b for _, b, _ in sol), 4),
+                            "bound": "per launch max(executed FP32 flops / FP32 peak, algorithmic bytes / HBM peak)",
+                            "fp32_peak_tflops": FP32_PEAK_TFLOPS, "hbm_peak_gbs": peak}
+                           if sol and all(k for _, _, k in sol) else None),
         "per_kernel": {k: {"GBps": round(v["bytes"] / (v["ms"] / 1e3) / 1e9, 1),
                            "ms_per_step": v["ms"] / nprof,
                            "launches_per_step": v["launches"] // nprof}
