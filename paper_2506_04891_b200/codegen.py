@@ -1914,8 +1914,10 @@ def generate_kernels(prog) -> list:
     C side can compile them in parallel."""
     with open(PRIMS) as f:
         prims = f.read()
-    if os.environ.get("LSQ_FAST_PHASE") == "1":
+    if os.environ.get("LSQ_FAST_PHASE") == "1":  # A/B runs: MUFU phases
         prims = "#define LSQ_FAST_PHASE 1\n" + prims
+    elif os.environ.get("LSQ_SINCOSPI") == "1":  # A/B runs: CUDA's sincospif
+        prims = "#define LSQ_SINCOSPI 1\n" + prims
     out = []
     for pi, mode in program_modes(prog):
         out.append((pi, mode, kernel_name(pi, mode), prims + "\n" + emit_kernel(prog, pi, mode) + "\n",
