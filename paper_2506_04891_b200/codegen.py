@@ -1918,6 +1918,8 @@ def generate_kernels(prog) -> list:
         prims = "#define LSQ_FAST_PHASE 1\n" + prims
     elif os.environ.get("LSQ_SINCOSPI") == "1":  # A/B runs: CUDA's sincospif
         prims = "#define LSQ_SINCOSPI 1\n" + prims
+    elif os.environ.get("LSQ_MUFU_REDUCED") == "1":  # A/B runs: MUFU after exact reduction
+        prims = "#define LSQ_MUFU_REDUCED 1\n" + prims
     out = []
     for pi, mode in program_modes(prog):
         out.append((pi, mode, kernel_name(pi, mode), prims + "\n" + emit_kernel(prog, pi, mode) + "\n",
