@@ -303,6 +303,54 @@ def _emit_u1_coupling(w, P, k, slot, comps):
         P.coup.add(w, names[ci], slot + pos, free)
 
 
+EULER_COUP = os.environ.get("LSQ_EULER_COUP", "1") != "0"
+
+
+def _pi1_chain(P, k):
+    """Packed chain whose .x + .y is sum over the pairs of register bit k of
+    Im(conj(lam_j) psi_j), j the member with the bit set: one FFMA2 per pair."""
+    acc = None
+    for i in range(1 << P.R):
+        if (i >> k) & 1:
+            continue
+        j = i | (1 << k)
+        a, b = f"v[1][{j}]", f"v[0][{j}]"
+        acc = f"vm_mj({a}, {b})" if acc is None else f"vf_mj({a}, {b}, {acc})"
+    return acc
+
+
+def _emit_euler_coupling_post(w, P, k):
+    """Couplings of a one-qubit group U = e^{id} D(a) R D(g) (D(x) = diag(1, e^{ix}), R a fixed
+    rotation: |U00| the same for every parameter value) taken at the Euler points instead of as
+    three Pauli components at the post-group point. Every derivative weight is
+    W = i (d' I + a' Pi1 + g' U Pi1 U^+), Pi1 = |1><1|, so the gradient only needs
+    P1 = Im <lam|Pi1|psi> after the group and Q1 = the same before it (where U Pi1 U^+ is Pi1
+    again): one FFMA2 per amplitude pair each, against six for the X, Y, Z components. This
+    part takes P1 (before the group is un-applied); _emit_euler_coupling_pre finishes."""
+    names = [P.coup.new(w) for _ in range(3)]
+    w(f"{{ const float2 t_ = {_pi1_chain(P, k)}; {names[0]} = {_scaled(P, '(t_.x + t_.y)')}; }}")
+    return names
+
+
+def _emit_euler_coupling_pre(w, P, k, slot, names, g, cmag):
+    """Q1 at the pre-group point, then the equivalent M' = [[i Z', i s], [t, 0]] the contraction
+    reads (slot floats 1, 3, 4, the layout of the X, Y, Z components): Z' = -2 P1 (Im<lam|psi>
+    = 0 over the row), (s, t) = mu (Re z, -Im z) with z = U01 conj(U11) and
+    mu = (Q1 - (|U11|^2 - |U01|^2) P1) / |z|^2, which reproduces 2 Re sum W_ab M_ab =
+    -2 (a' P1 + g' Q1) for every weight of the form above. |U11| = |U00| = cmag."""
+    c2 = float(cmag) ** 2
+    dz, zz = c2 - (1.0 - c2), c2 * (1.0 - c2)
+    w(f"{{ const float2 t_ = {_pi1_chain(P, k)}; const float q_ = {_scaled(P, '(t_.x + t_.y)')};")
+    q = "q_" if abs(dz) < 1e-12 else f"(q_ - {_f(dz)} * {names[0]})"
+    w(f"  const float mu_ = {q} * {_f(1.0 / zz)};")
+    w(f"  {names[1]} = mu_ * ({g}[2] * {g}[6] + {g}[3] * {g}[7]);")
+    w(f"  {names[2]} = mu_ * ({g}[2] * {g}[7] - {g}[3] * {g}[6]);")
+    w(f"  {names[0]} *= -2.f; }}")
+    free = [slot + q_ for q_ in range(8) if q_ not in (1, 3, 4)]
+    for nm, pos in zip(names, (1, 3, 4)):
+        P.coup.add(w, nm, slot + pos, free)
+
+
 def _emit_u1_struct(w, v, k, R, classes, g, dagger):
     """U (or U^+) from the table entry g (row-major re, im) on register bit k, emitting only
     the terms the structure allows: real entry -> one FFMA2, imaginary -> one FFMA2 on i x,
@@ -1008,9 +1056,21 @@ def _emit_ops(w, P, ph_idx, mode_bwd, nv):
             grp = P.prog.groups[gid]
             bits = [int(op[1])] + ([int(op[2])] if kind == S.OP_U2 else [])
             slot, moff = int(op[4]), int(op[5])
+            U = _group_const_matrix(grp, P.drop_phase)
+            direct = any(g.layer in getattr(P.prog, "direct_layers", ()) for g, _ in grp.gates)
+            ecoup = None  # Euler-point couplings (constant |U00| groups in the Euler tangent form)
             if mode_bwd and slot >= 0:
                 if kind == S.OP_U1:
-                    _emit_u1_coupling(w, P, bits[0], slot, u1_structure(grp)[1])
+                    classes, comps = u1_structure(grp)
+                    if (EULER_COUP and U is None and EULER_TAN and not direct and P.drop_phase
+                            and P.walsh_diag and "I" not in comps
+                            and all(c == "c" for row in classes for c in row)
+                            and not (TAN_ROT and P.tan_ok and is_rotation(grp))
+                            and u00_const_mag(grp) is not None
+                            and 1e-3 < u00_const_mag(grp) ** 2 < 1 - 1e-3):
+                        ecoup = _emit_euler_coupling_post(w, P, bits[0])
+                    else:
+                        _emit_u1_coupling(w, P, bits[0], slot, comps)
                 else:
                     csc = _scaled(P, "1.f")
                     fix_ = "" if csc == "1.f" else f"for (int e_ = 0; e_ < 8; ++e_) acc[e_] *= {csc}; "
@@ -1018,7 +1078,6 @@ def _emit_ops(w, P, ph_idx, mode_bwd, nv):
                         w(f"{{ float acc[8] = {{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}}; "
                           f"u2_coupling_row<{P.R}, {bits[0]}, {bits[1]}, {rr}>(v[0], v[1], acc); {fix_}"
                           f"warp_accumulate8<{P.NT}>(acc, wacc + {slot + 8 * rr}); }}")
-            U = _group_const_matrix(grp, P.drop_phase)
             uf = unit_form(U) if (U is not None and UNIT_CONST and P.walsh_diag) else None
             if uf is not None:
                 # U / kappa with entries in {0, +-1, +-i}; the vectors carry the deferred scale
@@ -1034,7 +1093,6 @@ def _emit_ops(w, P, ph_idx, mode_bwd, nv):
                 w(f"{{ const float* g_ = s_mat + {moff};")
                 general = all(c == "c" for row in classes for c in row)
                 cmag = u00_const_mag(grp) if general else None
-                direct = any(g.layer in getattr(P.prog, "direct_layers", ()) for g, _ in grp.gates)
                 if TAN_ROT and P.tan_ok and not direct and is_rotation(grp):
                     _emit_tan_rot(w, P, bits[0], "g_", nv if mode_bwd else 1, mode_bwd, classes)
                     if P.tan_count >= TAN_RENORM:
@@ -1043,12 +1101,16 @@ def _emit_ops(w, P, ph_idx, mode_bwd, nv):
                         and (cmag is not None or (P.tan_ok and EULER_BRANCH))):
                     _emit_euler_tan(w, P, bits[0], "g_", nv if mode_bwd else 1, mode_bwd, classes,
                                     branch=cmag is None)
+                    if ecoup is not None:
+                        _emit_euler_coupling_pre(w, P, bits[0], slot, ecoup, "g_", cmag)
+                        ecoup = None
                     if P.tan_count >= TAN_RENORM:
                         _renorm_rho(w, P, nv if mode_bwd else 1)
                 else:
                     for q in range(nv if mode_bwd else 1):
                         _emit_u1_struct(w, f"v[{q}]", bits[0], P.R, classes, "g_", mode_bwd)
                 w("}")
+                assert ecoup is None, "Euler-point coupling left unfinished"
             else:
                 if mode_bwd:
                     for q in range(nv):
@@ -1330,6 +1392,16 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
         w(f"(void)tp{k}; (void)gt{k}; (void)st{k};")
     w(f"const size_t rowbase = (size_t)row << {P.n};")
     w("const int t0 = cslot * A.tiles_per_cta, t_end = t0 + A.tiles_per_cta;")
+    skew_ns = int(os.environ.get("LSQ_SKEW_NS", "0"))
+    if skew_ns and mode in (MODE_BWD, MODE_TURN) + ((MODE_FWD,) if os.environ.get("LSQ_SKEW_FWD") == "1" else ()):
+        # experiment: de-phase the CTAs that share an SM (first wave only, later CTAs inherit the
+        # offset) so one computes while the other transposes
+        sm = int(os.environ.get("LSQ_SKEW_MODE", "1"))
+        cond = {1: "(blockIdx.x & 1)", 2: "((blockIdx.x / 148) & 1)",
+                3: f"((warpid_() / {P.NW}) & 1)"}[sm]
+        if sm == 3:
+            w("auto warpid_ = [] { unsigned r; asm volatile(\"mov.u32 %0, %%warpid;\" : \"=r\"(r)); return r; };")
+        w(f"if (blockIdx.x < {148 * minb} && {cond}) {{ for (int s_ = 0; s_ < {max(1, skew_ns // 1000)}; ++s_) __nanosleep(1000); }}")
     last = nph - 1
     # adjoint and turnaround kernels read their tile from the prefetch stage, where any layout
     # is free: an empty last phase (kept only so forward stores are coalesced) is skipped,
