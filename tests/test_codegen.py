@@ -86,3 +86,82 @@ def test_kernels_generate(cfg):
     assert len(names) == 2 * L  # forward per pass, adjoint per pass but the last, turnaround
     for _, _, name, src, _ in ks:
         assert f"void __launch_bounds__" in src and name in src
+
+
+_HOST_PRELUDE = r"""
+#include <cstdio>
+#include <cstdlib>
+struct float2 { float x, y; };
+static inline float2 make_float2(float x, float y) { float2 r; r.x = x; r.y = y; return r; }
+static inline float2 fx(float2 x, float s, float2 a) { return make_float2(a.x + s * x.x, a.y + s * x.y); }
+static inline float2 mx(float2 x, float s) { return make_float2(s * x.x, s * x.y); }
+static inline float2 fix(float2 x, float s, float2 a) { return make_float2(a.x - s * x.y, a.y + s * x.x); }
+static inline float2 cm(float ar, float ai, float2 x) { return fix(x, ai, mx(x, ar)); }
+"""
+
+
+def _euler_entry(U):
+    """floats 8..13 of a one-qubit group-table entry (csrc/lsq_common.cuh group_table_entry)"""
+    c = abs(U[0, 0])
+    ea = U[1, 0] * np.conj(U[0, 0])
+    ea /= abs(ea)
+    eg = U[1, 1] * np.conj(U[0, 0]) / c**2 * np.conj(ea)
+    return [c, abs(U[1, 0]) / c, ea.real, ea.imag, eg.real, eg.imag]
+
+
+@pytest.mark.parametrize("dagger", [False, True])
+@pytest.mark.parametrize("bits", [(0, 1, 2, 3), (2, 0), (3, 1, 0)])
+def test_euler_merged_block_on_host(tmp_path, bits, dagger):
+    """The emitted merged Euler block (codegen._emit_euler_merged), compiled as host C++ with
+    scalar stand-ins of the packed primitives, equals the product of the groups' unitaries
+    (global phases dropped, deferred scale P.sc) on random vectors."""
+    import shutil
+    import subprocess
+    import types
+
+    if shutil.which("g++") is None:
+        pytest.skip("no host compiler")
+    wl = make_workload(4)
+    prog = S.compile_circuit(wl.circuit, M=12, R=4, prefix=True, fold=True, split=True)
+    cand = [g for g in prog.groups if g.arity == 1 and not g.diag and not g.prefix
+            and codegen.u00_const_mag(g) is not None and len(g.gates) == 3]
+    grps = cand[: len(bits)]
+    assert len(grps) == len(bits)
+    rng = np.random.default_rng(5)
+    R, nvec = 4, 2
+    P = types.SimpleNamespace(NR=1 << R, R=R, sc=[1.0, 1.0], prog=prog)
+    run = [[S.OP_U1, b, -1, g.gid, -1, 16 * gi, 0, 0] for gi, (b, g) in enumerate(zip(bits, grps))]
+    w = codegen._W()
+    codegen._emit_euler_merged(w, P, run, nvec, dagger)
+    # group tables from random parameters
+    smat, Us = [], []
+    for g in grps:
+        U = np.eye(2, dtype=complex)
+        for gate, _ in g.gates:
+            k = len(gate.src)
+            U = (gate_matrix(gate.kind, [float(rng.uniform(-3, 3)) for _ in range(k)]) if k
+                 else gate_matrix(gate.kind)) @ U
+        ent = [0.0] * 16
+        for e in range(4):
+            ent[2 * e], ent[2 * e + 1] = U.flat[e].real, U.flat[e].imag
+        ent[8:14] = _euler_entry(U)
+        smat += ent
+        Us.append(U * np.exp(-1j * np.angle(U[0, 0])))  # global phase dropped
+    v = rng.normal(size=(nvec, 1 << R)) + 1j * rng.normal(size=(nvec, 1 << R))
+    init = "\n".join(f"v[{q}][{i}] = make_float2({float(v[q, i].real)!r}f, {float(v[q, i].imag)!r}f);"
+                     for q in range(nvec) for i in range(1 << R))
+    src = (_HOST_PRELUDE + f"int main() {{ float s_mat[{len(smat)}] = {{{', '.join(repr(float(np.float32(x))) + 'f' for x in smat)}}};\n"
+           f"float2 v[{nvec}][{1 << R}];\n{init}\n" + "\n".join(w.lines) +
+           f"\nfor (int q = 0; q < {nvec}; ++q) for (int i = 0; i < {1 << R}; ++i) printf(\"%.9g %.9g\\n\", v[q][i].x, v[q][i].y);\nreturn 0; }}\n")
+    (tmp_path / "m.cpp").write_text(src)
+    subprocess.run(["g++", "-O1", "-o", str(tmp_path / "m"), str(tmp_path / "m.cpp")], check=True)
+    out = subprocess.run([str(tmp_path / "m")], check=True, capture_output=True, text=True).stdout.split()
+    got = np.array(out, float).reshape(nvec, 1 << R, 2)
+    got = got[..., 0] + 1j * got[..., 1]
+    ref = v.copy()
+    for b, U in zip(bits, Us):
+        A = np.conj(U.T) if dagger else U
+        t = ref.reshape(nvec, 1 << (R - 1 - b), 2, 1 << b)  # register bit b of the index
+        ref = np.einsum("ij,qxjy->qxiy", A, t).reshape(nvec, 1 << R)
+    for q in range(nvec):
+        np.testing.assert_allclose(got[q] / P.sc[q], ref[q], atol=2e-5)
