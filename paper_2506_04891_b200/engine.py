@@ -166,7 +166,7 @@ def forward_program(circuit, prog, M=None, **kw):
     rf = forward_register_bits(prog.passes[0].M)
     if rf is None or rf == prog.passes[0].R or any(pp.M != prog.passes[0].M for pp in prog.passes):
         return None
-    pf = compile_circuit(circuit, M=M, R=rf, **kw)
+    pf = compile_circuit(circuit, M=M, R=rf, fwd_only=True, **kw)
     same = len(pf.passes) == len(prog.passes) and all(
         a.groups == b.groups and a.tile_wires == b.tile_wires for a, b in zip(pf.passes, prog.passes))
     return pf if same else None

@@ -516,7 +516,78 @@ def _lane_order(thread_bits, coalesced):
     return chosen + rest
 
 
-def schedule_phases(pp: PassPlan, groups, preds, n: int, R: int) -> None:
+PHASE_SEARCH = _os.environ.get("LSQ_PHASE_SEARCH", "1") != "0"
+PHASE_BEAM = int(_os.environ.get("LSQ_PHASE_BEAM", "6"))
+
+
+def _phase_closure(remaining, groups, ipreds, done, regs, loc):
+    """Non-diagonal groups of `remaining` (program order) a phase with register bits `regs` can
+    run after `done`: in-pass predecessors satisfied and wires on register bits; diagonal groups
+    run wherever their predecessors are done (they never need a register bit)."""
+    nd, opset = [], set()
+    for gid in remaining:
+        ip = ipreds[gid]
+        if not (ip <= done or ip <= (done | opset)):
+            continue
+        g = groups[gid]
+        if g.diag:
+            opset.add(gid)
+        elif loc[gid] <= regs:
+            opset.add(gid)
+            nd.append(gid)
+    return nd, opset
+
+
+def search_phase_registers(pp: PassPlan, groups, preds, n: int, R: int, low: set, last_free: bool):
+    """Register-bit sets of the pass's phases, fewest phases first: beam search over all
+    R-subsets of the tile's local bits per phase (the greedy scan packs a phase with the first
+    groups that fit, which on ladder circuits -- ECR / MS / CNOT chains -- leaves phases with two
+    or three groups and pays a transpose of every vector for each). The first phase keeps the
+    coalescing bits on lanes; with `last_free` a plan whose last phase does too is preferred
+    (forward programs store from it: otherwise an empty phase, i.e. one more transpose, follows).
+    Returns a list of register sets, or None (no non-diagonal group / search failed)."""
+    from itertools import combinations
+
+    in_pass = set(pp.groups)
+    ipreds = {gid: {p for p in preds[gid] if p in in_pass} for gid in pp.groups}
+    lop = {p: i for i, p in enumerate(sorted(n - 1 - w for w in pp.tile_wires))}
+    nd_all = [gid for gid in pp.groups if not groups[gid].diag]
+    if not nd_all:
+        return None
+    loc = {gid: frozenset(lop[n - 1 - w] for w in groups[gid].wires) for gid in nd_all}
+    useful = sorted(set().union(*(loc[g] for g in nd_all)))
+    r = min(R, len(useful))
+    allsets = [frozenset(c) for c in combinations(useful, r)]
+    firstsets = [s for s in allsets if not (s & low)]
+    if not firstsets:  # fewer than R non-coalescing bits in use: any subset of them
+        hi = [b for b in useful if b not in low]
+        firstsets = [frozenset(c) for c in combinations(hi, min(r, len(hi)))] if hi else []
+    cost = {gid: _fp_cost(groups[gid]) for gid in pp.groups}
+    states = [(frozenset(), ())]  # (done groups incl. diagonal ones, plan)
+    for depth in range(4 * len(nd_all) + 2):
+        fin = [st for st in states if all(g in st[0] for g in nd_all)]
+        if fin:
+            if last_free:
+                fin.sort(key=lambda st: bool(st[1][-1] & low))
+            return [set(x) for x in fin[0][1]]
+        nxt = {}
+        for done, plan in states:
+            remaining = [g for g in pp.groups if g not in done]
+            for regs in (firstsets if depth == 0 else allsets):
+                nd, opset = _phase_closure(remaining, groups, ipreds, done, regs, loc)
+                if not nd:
+                    continue
+                d2 = done | opset
+                if d2 not in nxt:
+                    nxt[d2] = plan + (regs,)
+        if not nxt:
+            return None
+        ranked = sorted(nxt.items(), key=lambda kv: -sum(cost[g] for g in kv[0]))
+        states = ranked[:PHASE_BEAM]
+    return None
+
+
+def schedule_phases(pp: PassPlan, groups, preds, n: int, R: int, last_free: bool = False) -> None:
     M = pp.M
     phys = sorted(n - 1 - w for w in pp.tile_wires)
     pp.phys_of_local = phys
@@ -525,45 +596,68 @@ def schedule_phases(pp: PassPlan, groups, preds, n: int, R: int) -> None:
     coal = COAL if (M - R) >= COAL else 0
     low = set(range(coal))
     in_pass = set(pp.groups)
-    ext_done = set()  # groups outside this pass count as satisfied
-    remaining = list(pp.groups)
-    done: set = set()
-    phases = []
-    first = True
-    while remaining:
-        regs: set = set()
-        ops = []
-        opset = set()
-        for gid in remaining:
-            g = groups[gid]
-            if not {p for p in preds[gid] if p in in_pass} <= (done | opset):
-                continue
-            if g.diag:
-                ops.append(gid)
-                opset.add(gid)
-                continue
-            need = {loc(w) for w in g.wires} - regs
-            if first and need & low:
-                continue
-            if len(regs) + len(need) <= R:
-                regs |= need
-                ops.append(gid)
-                opset.add(gid)
-        if not ops and not first:
-            raise RuntimeError("phase scheduler made no progress")
-        ops = _defer_diagonal(ops, regs, remaining, groups,
-                              lambda w: pp.local_of_phys.get(n - 1 - w, -1))
-        opset = set(ops)
-        phases.append([regs, ops])
-        done |= opset
-        remaining = [g for g in remaining if g not in opset]
-        first = False
-    if not phases:
-        phases.append([set(), []])
-    if coal and (phases[-1][0] & low):
-        phases.append([set(), []])
-    if coal and (phases[0][0] & low):  # cannot happen (first-phase rule) but keep it safe
-        phases.insert(0, [set(), []])
+
+    def build(plan):
+        """phases [[register bits, ops]] with the greedy scan (plan None) or with the register
+        bits of every phase given by the searched plan"""
+        remaining = list(pp.groups)
+        done: set = set()
+        phases = []
+        first = True
+        while remaining:
+            fixed = plan[len(phases)] if plan is not None and len(phases) < len(plan) else None
+            regs: set = set()
+            ops = []
+            opset = set()
+            for gid in remaining:
+                g = groups[gid]
+                if not {p for p in preds[gid] if p in in_pass} <= (done | opset):
+                    continue
+                if g.diag:
+                    ops.append(gid)
+                    opset.add(gid)
+                    continue
+                need = {loc(w) for w in g.wires} - regs
+                if fixed is not None:  # searched plan: the phase's register bits are given
+                    if {loc(w) for w in g.wires} <= fixed:
+                        regs |= need
+                        ops.append(gid)
+                        opset.add(gid)
+                    continue
+                if first and need & low:
+                    continue
+                if len(regs) + len(need) <= R:
+                    regs |= need
+                    ops.append(gid)
+                    opset.add(gid)
+            if not ops and not first:
+                raise RuntimeError("phase scheduler made no progress")
+            ops = _defer_diagonal(ops, regs, remaining, groups,
+                                  lambda w: pp.local_of_phys.get(n - 1 - w, -1))
+            opset = set(ops)
+            phases.append([regs, ops])
+            done |= opset
+            remaining = [g for g in remaining if g not in opset]
+            first = False
+        if not phases:
+            phases.append([set(), []])
+        if coal and (phases[-1][0] & low):
+            phases.append([set(), []])
+        if coal and (phases[0][0] & low):  # cannot happen (first-phase rule) but keep it safe
+            phases.insert(0, [set(), []])
+        return phases
+
+    phases = build(None)
+    if PHASE_SEARCH and len(phases) > 2:
+        plan = search_phase_registers(pp, groups, preds, n, R, low, last_free)
+        if plan is not None:
+            # transposes a kernel pays: forward-only programs store from the last phase (an
+            # empty coalescing phase counts); adjoint kernels read their tile from the stage in
+            # any layout, so an empty last phase costs them nothing
+            cost = (lambda ph: len(ph)) if last_free else (lambda ph: len(ph) - (not ph[-1][1]))
+            cand = build(plan)
+            if cost(cand) < cost(phases):
+                phases = cand
     out = []
     for i, (regs, ops) in enumerate(phases):
         ops = _sink_diagonal(ops, groups)
@@ -706,7 +800,7 @@ def observable_masks(perms, n: int):
 
 def compile_circuit(circuit, M: int | None = None, R: int | None = None, isolate=(),
                     prefix: bool = False, fold: bool = False, split: bool = False, direct=(),
-                    split_layers=()) -> Program:
+                    split_layers=(), fwd_only: bool = False) -> Program:
     """Compile a (reference-compatible) circuit into a pass program.
 
     Planner variants (layer indices): `isolate` -- executed with pass boundaries of their own
@@ -714,6 +808,8 @@ def compile_circuit(circuit, M: int | None = None, R: int | None = None, isolate
     `direct` -- one-qubit groups containing a gate of these layers are applied in the direct
     8-op form, not the Euler tangent form (DIRECT); `split_layers` -- one-qubit groups with a
     gate of these (diagonal) layers are split into diagonal runs and the rest (SPLIT).
+    `fwd_only`: the program only provides forward kernels (engine.forward_program), so the phase
+    search prefers plans whose LAST phase keeps the coalescing bits on lanes (forward stores).
     """
     n = int(circuit.n)
     gates = flatten_gates(circuit)
@@ -760,7 +856,7 @@ def compile_circuit(circuit, M: int | None = None, R: int | None = None, isolate
             r = default_r(pp.M) if R is None else min(R, pp.M)
             if need2 and r < 2:
                 r = min(2, pp.M)
-            schedule_phases(pp, grp, preds, n, r)
+            schedule_phases(pp, grp, preds, n, r, last_free=fwd_only)
         off = len(groups)
         for g in grp:
             g.gid += off
