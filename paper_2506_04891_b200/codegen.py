@@ -1360,11 +1360,13 @@ class _Rot:
     reuse a dirty one, so a two-vector exchange costs two barriers instead of four and a
     one-vector exchange one instead of two."""
 
-    def __init__(self, P, nstage, late=True):
+    def __init__(self, P, nstage, late=True, bufs=None):
         # late: the stage is free during the tile (prefetch issued after the last transpose);
         # otherwise only the stage's unused second vector (turnaround kernels) joins s_x
         self.late = late
-        if late:
+        if bufs is not None:
+            self.bufs = list(bufs)
+        elif late:
             self.bufs = ["s_x", "s_stage", f"(s_stage + {1 << P.M})"][: 1 + nstage]
         else:
             self.bufs = ["s_x", f"(s_stage + {1 << P.M})"]
@@ -1415,6 +1417,23 @@ def stage_vectors(prog, pi: int, mode: int) -> int:
     return 0
 
 
+# forward kernels with ONE tile buffer: the prefetch stage and the exchange buffer are the same
+# 2^M amplitudes (the next tile is prefetched after the last transpose, like the adjoint
+# kernels' late prefetch), so a CTA needs 32 KB + tables at M = 12 instead of 64 KB and the
+# 128-thread forward CTAs run 4 per SM (register-limited) instead of 3 (shared-memory-limited)
+FWD_SINGLE = os.environ.get("LSQ_FWD_SINGLE", "1") != "0"
+
+
+def fwd_single(prog, pi: int, mode: int) -> bool:
+    return bool(FWD_SINGLE and mode == MODE_FWD and stage_vectors(prog, pi, mode) > 0)
+
+
+def stage_alloc(prog, pi: int, mode: int) -> int:
+    """Stage vectors the C side allocates after the fixed shared-memory layout (lsq_program_jit):
+    none for single-buffer forward kernels, whose stage aliases the exchange buffer."""
+    return 0 if fwd_single(prog, pi, mode) else stage_vectors(prog, pi, mode)
+
+
 def emit_kernel(prog, pi: int, mode: int) -> str:
     P = _Pass(prog, pi)
     P.coup = _Coup(P)
@@ -1440,6 +1459,9 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
             rot = _Rot(P, 2)
         elif mode == MODE_TURN and nph > 1 and os.environ.get("LSQ_ROT_TURN", "1") != "0":
             rot = _Rot(P, 2, late=False)  # psi-only stage: its lambda half is a spare buffer
+        elif mode == MODE_FWD and fwd_single(prog, pi, mode):
+            if nph > 1:  # the one buffer is stage and exchange buffer: late prefetch
+                rot = _Rot(P, 1, bufs=["s_stage"])
         elif mode == MODE_FWD and nph >= int(os.environ.get("LSQ_ROT_FWD_PHASES", "99")):
             # forward kernels: measured neutral (one vector: the early prefetch overlap matters
             # as much as the saved barrier), so off by default
@@ -1475,7 +1497,10 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
     # generic LD) for the stage reads
     off = (8 << P.M) + 4 * ((matf + 3) & ~3) + 4 * ((P.NW * (slotf + 8) + 3) & ~3) + 8 * 34 + 4 * P.NW * 32
     off = (off + 15) & ~15
-    w(f"float2* s_stage = reinterpret_cast<float2*>(smem_raw + {off});")
+    if fwd_single(prog, pi, mode):
+        w("float2* s_stage = s_x;  // single tile buffer: prefetch stage == exchange buffer")
+    else:
+        w(f"float2* s_stage = reinterpret_cast<float2*>(smem_raw + {off});")
     # the prefix vectors live in the first 8*n bytes of the exchange buffer's tail region: use a
     # dedicated register-free path -- they are read from global (L1-cached, 16 B per wire)
     w("const int tid = threadIdx.x, warp = tid >> 5;")
@@ -1621,7 +1646,7 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
             w("cp_async_wait_all();")
             w("__syncthreads();")
             emit_stage_read(k)
-            rot.dirty = set(rot.bufs[1:])  # stage vectors read without a barrier
+            rot.dirty = {b for b in rot.bufs if b != "s_x"}  # stage vectors read without a barrier
         elif prefetch:
             w("cp_async_wait_all();")
             w("__syncthreads();")
@@ -2121,7 +2146,7 @@ def generate_kernels(prog) -> list:
     out = []
     for pi, mode in program_modes(prog):
         out.append((pi, mode, kernel_name(pi, mode), prims + "\n" + emit_kernel(prog, pi, mode) + "\n",
-                    stage_vectors(prog, pi, mode)))
+                    stage_alloc(prog, pi, mode)))
     return out
 
 

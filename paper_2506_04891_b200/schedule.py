@@ -376,6 +376,45 @@ def _greedy_pass(order, groups, preds, done, base, M, first_forced=None):
     return S, chosen, work
 
 
+PASS_BEAM = int(_os.environ.get("LSQ_PASS_BEAM", "8"))  # 1: greedy pass partition (round 1)
+
+
+def _search_passes(groups, preds, remaining, done, base, M, seeds):
+    """Pass partition with the fewest HBM round trips: beam search over sequences of greedy
+    passes (one candidate per seed group, as the greedy partition tries them), ranked by the
+    non-diagonal work done so far. The greedy partition takes the heaviest pass at every step,
+    which on ladder circuits strands a few groups in extra, nearly empty passes at the end
+    (cfg4 at M = 12: 10 passes greedy, 8 searched). Returns [(tile wires, groups)] or None."""
+    work = {gid: (0 if groups[gid].diag else 1 + len(groups[gid].gates)) for gid in remaining}
+    total = set(remaining)
+    states = [(frozenset(done), ())]
+    for _depth in range(4 * len(remaining) + 2):
+        fin = [st for st in states if total <= st[0]]
+        if fin:
+            # fewest passes reached: prefer the most even split of the work
+            fin.sort(key=lambda st: max(sum(work[g] for g in ch) for _, ch in st[1]))
+            return [(set(S_), list(ch)) for S_, ch in fin[0][1]]
+        nxt = {}
+        for dn, plan in states:
+            rem = [g for g in remaining if g not in dn]
+            dset = set(dn)
+            cands = [_greedy_pass(rem, groups, preds, dset, base, M)]
+            ready = [g for g in rem if preds[g] <= dset and not groups[g].diag][:seeds]
+            for gid in ready[1:]:
+                cands.append(_greedy_pass(rem, groups, preds, dset, base, M, first_forced=gid))
+            for S_, chosen, _w in cands:
+                if not chosen:
+                    continue
+                d2 = dn | frozenset(chosen)
+                if d2 not in nxt:
+                    nxt[d2] = plan + ((frozenset(S_), tuple(chosen)),)
+        if not nxt:
+            return None
+        ranked = sorted(nxt.items(), key=lambda kv: -sum(work.get(g, 0) for g in kv[0]))
+        states = ranked[:PASS_BEAM]
+    return None
+
+
 def schedule_passes(groups, n, M, seeds: int = 12, skip=()) -> list[PassPlan]:
     """Greedy tile-pass partition; tries a few seeds per pass and keeps the one that
     schedules the most non-diagonal work. Groups in `skip` (the synthesized product-state
@@ -389,16 +428,22 @@ def schedule_passes(groups, n, M, seeds: int = 12, skip=()) -> list[PassPlan]:
         return [PassPlan(set(range(n)), remaining, M=n)]
     # wires at the lowest physical bits (coalescing); leave room for one 2-qubit gate
     base = {n - 1 - p for p in range(min(COAL, max(0, M - 2)))}
+    plan = _search_passes(groups, preds, remaining, done, base, M, seeds) if PASS_BEAM > 1 else None
+    step = 0
     while remaining:
-        best = _greedy_pass(remaining, groups, preds, done, base, M)
-        ready_nd = [
-            gid for gid in remaining if preds[gid] <= done and not groups[gid].diag
-        ][:seeds]
-        for gid in ready_nd[1:]:
-            cand = _greedy_pass(remaining, groups, preds, done, base, M, first_forced=gid)
-            if cand[2] > best[2]:
-                best = cand
-        S, chosen, _ = best
+        if plan is not None:
+            S, chosen = set(plan[step][0]), list(plan[step][1])
+            step += 1
+        else:
+            best = _greedy_pass(remaining, groups, preds, done, base, M)
+            ready_nd = [
+                gid for gid in remaining if preds[gid] <= done and not groups[gid].diag
+            ][:seeds]
+            for gid in ready_nd[1:]:
+                cand = _greedy_pass(remaining, groups, preds, done, base, M, first_forced=gid)
+                if cand[2] > best[2]:
+                    best = cand
+            S, chosen, _ = best
         if not chosen:
             raise RuntimeError("scheduler made no progress")
         # fill the tile to exactly M wires with the wires needed soonest
@@ -518,6 +563,7 @@ def _lane_order(thread_bits, coalesced):
 
 PHASE_SEARCH = _os.environ.get("LSQ_PHASE_SEARCH", "1") != "0"
 PHASE_BEAM = int(_os.environ.get("LSQ_PHASE_BEAM", "6"))
+FIRST_FREE = _os.environ.get("LSQ_FIRST_FREE", "1") != "0"
 
 
 def _phase_closure(remaining, groups, ipreds, done, regs, loc):
@@ -538,7 +584,8 @@ def _phase_closure(remaining, groups, ipreds, done, regs, loc):
     return nd, opset
 
 
-def search_phase_registers(pp: PassPlan, groups, preds, n: int, R: int, low: set, last_free: bool):
+def search_phase_registers(pp: PassPlan, groups, preds, n: int, R: int, low: set, last_free: bool,
+                           first_free: bool = False):
     """Register-bit sets of the pass's phases, fewest phases first: beam search over all
     R-subsets of the tile's local bits per phase (the greedy scan packs a phase with the first
     groups that fit, which on ladder circuits -- ECR / MS / CNOT chains -- leaves phases with two
@@ -558,7 +605,7 @@ def search_phase_registers(pp: PassPlan, groups, preds, n: int, R: int, low: set
     useful = sorted(set().union(*(loc[g] for g in nd_all)))
     r = min(R, len(useful))
     allsets = [frozenset(c) for c in combinations(useful, r)]
-    firstsets = [s for s in allsets if not (s & low)]
+    firstsets = allsets if first_free else [s for s in allsets if not (s & low)]
     if not firstsets:  # fewer than R non-coalescing bits in use: any subset of them
         hi = [b for b in useful if b not in low]
         firstsets = [frozenset(c) for c in combinations(hi, min(r, len(hi)))] if hi else []
@@ -596,6 +643,9 @@ def schedule_phases(pp: PassPlan, groups, preds, n: int, R: int, last_free: bool
     coal = COAL if (M - R) >= COAL else 0
     low = set(range(coal))
     in_pass = set(pp.groups)
+    # forward-only programs read their tile from the prefetch stage, where any layout is as
+    # good as another: only the LAST phase (global stores) must keep the coalescing bits on lanes
+    first_free = bool(last_free and FIRST_FREE and M <= 13)
 
     def build(plan):
         """phases [[register bits, ops]] with the greedy scan (plan None) or with the register
@@ -624,7 +674,7 @@ def schedule_phases(pp: PassPlan, groups, preds, n: int, R: int, last_free: bool
                         ops.append(gid)
                         opset.add(gid)
                     continue
-                if first and need & low:
+                if first and need & low and not first_free:
                     continue
                 if len(regs) + len(need) <= R:
                     regs |= need
@@ -643,25 +693,28 @@ def schedule_phases(pp: PassPlan, groups, preds, n: int, R: int, last_free: bool
             phases.append([set(), []])
         if coal and (phases[-1][0] & low):
             phases.append([set(), []])
-        if coal and (phases[0][0] & low):  # cannot happen (first-phase rule) but keep it safe
+        if coal and (phases[0][0] & low) and not first_free:  # cannot happen (first-phase rule)
             phases.insert(0, [set(), []])
         return phases
 
+    ff, first_free = first_free, False
     phases = build(None)
     if PHASE_SEARCH and len(phases) > 2:
-        plan = search_phase_registers(pp, groups, preds, n, R, low, last_free)
-        if plan is not None:
-            # transposes a kernel pays: forward-only programs store from the last phase (an
-            # empty coalescing phase counts); adjoint kernels read their tile from the stage in
-            # any layout, so an empty last phase costs them nothing
-            cost = (lambda ph: len(ph)) if last_free else (lambda ph: len(ph) - (not ph[-1][1]))
-            cand = build(plan)
-            if cost(cand) < cost(phases):
-                phases = cand
+        # transposes a kernel pays: forward-only programs store from the last phase (an empty
+        # coalescing phase counts); adjoint kernels read their tile from the stage in any
+        # layout, so an empty last phase costs them nothing
+        cost = (lambda ph: len(ph)) if last_free else (lambda ph: len(ph) - (not ph[-1][1]))
+        for free in ((False, True) if ff else (False,)):
+            first_free = free
+            plan = search_phase_registers(pp, groups, preds, n, R, low, last_free, free)
+            if plan is not None:
+                cand = build(plan)
+                if cost(cand) < cost(phases):
+                    phases = cand
     out = []
     for i, (regs, ops) in enumerate(phases):
         ops = _sink_diagonal(ops, groups)
-        coalesced = coal and (i == 0 or i == len(phases) - 1)
+        coalesced = coal and (i == 0 or i == len(phases) - 1) and not (set(regs) & low)
         regs = sorted(regs)
         pool = [b for b in range(M) if b not in regs and not (coalesced and b in low)]
         # pad register bits, preferring high local bits (keeps low bits on lanes)
