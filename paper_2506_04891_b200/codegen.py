@@ -1471,7 +1471,8 @@ def emit_kernel(prog, pi: int, mode: int) -> str:
     if mode == MODE_FWD and P.R >= 5:
         # forward kernels with 32 amplitudes per thread: 128 registers (64 data), 4 CTAs of 128
         # threads per SM (LSQ_MINB_FWD5 overrides, A/B runs)
-        minb = int(os.environ.get("LSQ_MINB_FWD5", "4"))
+        # (128-register budget whatever the tile size: M = 13 has 256 threads -> 2 CTAs/SM)
+        minb = int(os.environ.get("LSQ_MINB_FWD5", str(max(1, min(4, 65536 // (P.NT * 128))))))
     elif mode == MODE_FWD:
         # forward kernels: an 80-register budget (measured: 256-thread tiles at 3 CTAs/SM beat 2,
         # 128-thread tiles at 6 beat 4 -- occupancy wins over a few spills)

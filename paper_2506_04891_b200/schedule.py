@@ -385,6 +385,8 @@ def _search_passes(groups, preds, remaining, done, base, M, seeds):
     non-diagonal work done so far. The greedy partition takes the heaviest pass at every step,
     which on ladder circuits strands a few groups in extra, nearly empty passes at the end
     (cfg4 at M = 12: 10 passes greedy, 8 searched). Returns [(tile wires, groups)] or None."""
+    if not remaining:
+        return None
     work = {gid: (0 if groups[gid].diag else 1 + len(groups[gid].gates)) for gid in remaining}
     total = set(remaining)
     states = [(frozenset(done), ())]
@@ -392,7 +394,7 @@ def _search_passes(groups, preds, remaining, done, base, M, seeds):
         fin = [st for st in states if total <= st[0]]
         if fin:
             # fewest passes reached: prefer the most even split of the work
-            fin.sort(key=lambda st: max(sum(work[g] for g in ch) for _, ch in st[1]))
+            fin.sort(key=lambda st: max((sum(work[g] for g in ch) for _, ch in st[1]), default=0))
             return [(set(S_), list(ch)) for S_, ch in fin[0][1]]
         nxt = {}
         for dn, plan in states:

@@ -209,3 +209,34 @@ def test_reference_circuit_objects_compile_by_duck_typing(cfg):
     res = Emulator(prog).gradient(wl.theta, wl.x, 3, wl.weights)
     ref = orc.gradient(wl.circuit, wl.theta, wl.x, batch=3, weights=wl.weights)
     _cmp(res, ref)
+
+
+@pytest.mark.parametrize("cfg", [2, 3, 4, 5])
+def test_all_variants_compile_and_emulate(cfg):
+    """The compile of tests/test_gpu_parity.py::test_all_variants_forced_vs_oracle (every
+    non-default variant at once: isolated segments whose groups are all synthesized or folded
+    leave a segment with nothing to schedule) on the CPU, at n=12 for the pass / phase searches
+    and at n=6 on the emulator against the oracle."""
+    from paper_2506_04891_b200 import planner as P
+
+    def variants(circ, n):
+        K = P.KernelKind
+        sel = {K.DIRECT: [], K.SPLIT: [], K.ISOLATED: []}
+        for i, layer in enumerate(circ.layers):
+            av = P.applicable_variants(layer, n)
+            k = K.DIRECT if K.DIRECT in av else K.SPLIT if K.SPLIT in av else K.ISOLATED if i < 6 else None
+            if k is not None:
+                sel[k].append(i)
+        return dict(isolate=sel[K.ISOLATED], direct=sel[K.DIRECT], split_layers=sel[K.SPLIT])
+
+    wl = make_workload(cfg, n=12, batch=1)
+    for R in (4, 5):
+        prog = S.compile_circuit(wl.circuit, M=9, R=R, prefix=True, fold=True, split=True,
+                                 fwd_only=R == 5, **variants(wl.circuit, 12))
+        seen = sorted(g for pp in prog.passes for g in pp.groups)
+        assert len(seen) == len(set(seen))
+    wl = make_workload(cfg, n=6, batch=2)
+    prog = S.compile_circuit(wl.circuit, M=4, R=2, prefix=True, fold=True, split=True, **variants(wl.circuit, 6))
+    res = Emulator(prog).gradient(wl.theta, wl.x, 2, wl.weights)
+    ref = orc.gradient(wl.circuit, wl.theta, wl.x, batch=2, weights=wl.weights)
+    _cmp(res, ref, atol=1e-8)
