@@ -384,6 +384,32 @@ def test_all_variants_forced_vs_oracle(cfg, n):
     check(res, ref, what=f"cfg{cfg}_all_variants")
 
 
+@pytest.mark.parametrize("cfg,n", [(4, 14), (3, 14), (5, 14)])
+@pytest.mark.parametrize("knobs", [
+    dict(EULER_MERGE=0, FWD_SINGLE=False, PASS_BEAM=1, PHASE_SEARCH=False),  # round-1 compiler
+    dict(EULER_MERGE=3, FWD_SINGLE=True, PASS_BEAM=8, PHASE_SEARCH=True),  # longer runs only
+    dict(EULER_MERGE=2, FWD_SINGLE=False, PASS_BEAM=8, PHASE_SEARCH=False),
+], ids=["all_off", "merge3", "beam_only"])
+def test_compiler_knobs_vs_oracle(cfg, n, knobs, monkeypatch):
+    """The searched pass / phase partitions, the merged Euler diagonals and the single-buffer
+    forward kernels against the oracle with each of them switched off or varied (the defaults are
+    what every other test runs), on multi-pass programs (M = 10)."""
+    from paper_2506_04891_b200 import codegen, schedule
+
+    monkeypatch.setattr(codegen, "EULER_MERGE", knobs["EULER_MERGE"])
+    monkeypatch.setattr(codegen, "FWD_SINGLE", knobs["FWD_SINGLE"])
+    monkeypatch.setattr(schedule, "PASS_BEAM", knobs["PASS_BEAM"])
+    monkeypatch.setattr(schedule, "PHASE_SEARCH", knobs["PHASE_SEARCH"])
+    wl = make_workload(cfg, n=n, batch=3)
+    eng = Engine(wl.circuit, M=10)
+    assert len(eng.program.passes) > 1
+    r = eng.fwd_bwd(wl.theta, wl.x, batch=3, weights=wl.weights)
+    ref = orc.gradient(wl.circuit, wl.theta, wl.x, batch=3, weights=wl.weights)
+    np.testing.assert_allclose(r["zq"].cpu().numpy(), ref["zq"], atol=Z_TOL)
+    assert_grads_close(_angles(r["grads"].cpu().numpy(), r["encoding_grads"].cpu().numpy()),
+                       _angles(ref["grads"], ref["encoding_grads"]), what=f"cfg{cfg}_knobs")
+
+
 def test_choose_tile_bits_and_plan_replay():
     """Measured tile exponent (bench default) replayed through the public gradient()."""
     from paper_2506_04891_b200 import planner as P
