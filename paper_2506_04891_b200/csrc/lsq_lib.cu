@@ -7,6 +7,7 @@
 #include <limits.h>
 #include <nvrtc.h>
 #include <stdlib.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <cstdio>
@@ -735,7 +736,11 @@ int jit_compile(const std::string& src, const std::string& cache_dir, std::strin
   R.cubin(prog, &cubin[0]);
   R.destroy(&prog);
   if (!key.empty()) {
-    std::string tmp = key + ".tmp" + std::to_string((unsigned long long)std::hash<std::thread::id>{}(std::this_thread::get_id()));
+    // unique per process AND thread: the ranks of a torchrun job compile the same kernels at the
+    // same time into one cache directory, and equal thread ids across processes would let one
+    // rank truncate the file another is about to rename
+    std::string tmp = key + ".tmp" + std::to_string((long long)getpid()) + "_" +
+                      std::to_string((unsigned long long)std::hash<std::thread::id>{}(std::this_thread::get_id()));
     std::ofstream f(tmp, std::ios::binary);
     if (f) {
       f.write(cubin.data(), (std::streamsize)cubin.size());
