@@ -614,6 +614,7 @@ def _emit_euler_merged(w, P, run, nvec, dagger):
     need no run-time rho_. Adjoint: conj(post) first, R^+, conj(pre)."""
     k = len(run)
     bits = [int(op[1]) for op in run]
+    assert len(set(bits)) == k, "merged Euler run on repeated register bits"
     w("{")
     w.ind += 1
     for gi, op in enumerate(run):
@@ -1126,11 +1127,16 @@ def _emit_ops(w, P, ph_idx, mode_bwd, nv):
         EULER_MERGE), else None; a group a diagonal run folds into stays on the fold path"""
         if not EULER_MERGE:
             return None
-        j = idx
+        j, bits = idx, set()
         while j < len(seq) and euler_plain(seq[j]):
             nx = seq[j + 1] if j + 1 < len(seq) else None
             if mode_bwd and foldable(nx, seq[j]):
                 break
+            # distinct register bits only: two groups of one wire can be neighbours when what
+            # separates them emits no op (an identity permutation, e.g. ECR applied twice)
+            if int(seq[j][1]) in bits:
+                break
+            bits.add(int(seq[j][1]))
             j += 1
         return seq[idx:j] if j - idx >= max(2, EULER_MERGE) else None
 

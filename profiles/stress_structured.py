@@ -17,12 +17,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from oracle import layersim_oracle as orc  # noqa: E402
 from paper_2506_04891_b200.circuits import Circuit, Layer, Role, all_qubits, chain_pairs, explicit, ring_pairs  # noqa: E402
-from paper_2506_04891_b200.engine import Engine  # noqa: E402
 from paper_2506_04891_b200.gates import GATE_TRAITS, GateKind  # noqa: E402
 
-cases = int(sys.argv[1]) if len(sys.argv) > 1 else 40
-seed = int(sys.argv[2]) if len(sys.argv) > 2 else 0
-rng = np.random.default_rng(seed)
+rng = np.random.default_rng(0)  # reseeded by main() / the CPU test that imports build()
 
 
 def npos(pat, n):
@@ -83,34 +80,48 @@ def build(n):
     return fam, Circuit(n, layers)
 
 
-worst, bad, t0 = 0.0, 0, time.time()
-for c in range(cases):
+def draw_case():
+    """(family, circuit, n, tile exponent M, batch) of the next random case"""
     n = int(rng.integers(9, 15))
     M = int(rng.integers(7, min(n, 12)))
     fam, circ = build(n)
-    B = int(rng.integers(1, 4))
-    theta = rng.uniform(-3, 3, circ.trainable_count)
-    x = rng.uniform(0, 3, (B, circ.encoding_count))
-    w = rng.normal(size=n)
-    eng = Engine(circ, M=M)
-    r = eng.fwd_bwd(theta, x, batch=B, weights=w)
-    ref = orc.gradient(circ, theta, x, batch=B, weights=w)
-    zerr = float(np.abs(r["zq"].cpu().numpy() - ref["zq"]).max())
-    host = lambda t: np.zeros((B, 0)) if t is None else t.cpu().numpy()  # noqa: E731 (no such angles)
-    g = np.concatenate([host(r["grads"]), host(r["encoding_grads"])], 1)
-    gr = np.concatenate([ref["grads"], ref["encoding_grads"]], 1)
-    if gr.size == 0:
-        a2 = 0.0
-    elif np.abs(gr).max() > 1e-9:
-        a2 = float(np.max(np.abs(g - gr) / np.maximum(np.abs(gr), 1e-2 * np.abs(gr).max())))
-    else:  # structurally zero gradients: absolute
-        a2 = float(np.abs(g).max())
-    ok = zerr <= 1e-5 and a2 <= 1e-4
-    worst = max(worst, a2)
-    bad += not ok
-    print(f"case {c:3d} {fam:4s} n={n:2d} M={M:2d} B={B} layers={len(circ.layers):2d} passes={len(eng.program.passes):2d} "
-          f"phases={sum(len(p.phases) for p in eng.program.passes):3d} zq_err={zerr:.1e} a2={a2:.1e} {'ok' if ok else 'FAIL'}",
-          flush=True)
-    del eng
-print(f"{cases} cases, {bad} failures, worst A2 {worst:.2e}, {time.time() - t0:.0f} s")
-sys.exit(1 if bad else 0)
+    return fam, circ, n, M, int(rng.integers(1, 4))
+
+
+def main(cases, seed):
+    global rng
+    from paper_2506_04891_b200.engine import Engine
+
+    rng = np.random.default_rng(seed)
+    worst, bad, t0 = 0.0, 0, time.time()
+    for c in range(cases):
+        fam, circ, n, M, B = draw_case()
+        theta = rng.uniform(-3, 3, circ.trainable_count)
+        x = rng.uniform(0, 3, (B, circ.encoding_count))
+        w = rng.normal(size=n)
+        eng = Engine(circ, M=M)
+        r = eng.fwd_bwd(theta, x, batch=B, weights=w)
+        ref = orc.gradient(circ, theta, x, batch=B, weights=w)
+        zerr = float(np.abs(r["zq"].cpu().numpy() - ref["zq"]).max())
+        host = lambda t: np.zeros((B, 0)) if t is None else t.cpu().numpy()  # noqa: E731 (no such angles)
+        g = np.concatenate([host(r["grads"]), host(r["encoding_grads"])], 1)
+        gr = np.concatenate([ref["grads"], ref["encoding_grads"]], 1)
+        if gr.size == 0:
+            a2 = 0.0
+        elif np.abs(gr).max() > 1e-9:
+            a2 = float(np.max(np.abs(g - gr) / np.maximum(np.abs(gr), 1e-2 * np.abs(gr).max())))
+        else:  # structurally zero gradients: absolute
+            a2 = float(np.abs(g).max())
+        ok = zerr <= 1e-5 and a2 <= 1e-4
+        worst = max(worst, a2)
+        bad += not ok
+        print(f"case {c:3d} {fam:4s} n={n:2d} M={M:2d} B={B} layers={len(circ.layers):2d} passes={len(eng.program.passes):2d} "
+              f"phases={sum(len(p.phases) for p in eng.program.passes):3d} zq_err={zerr:.1e} a2={a2:.1e} {'ok' if ok else 'FAIL'}",
+              flush=True)
+        del eng
+    print(f"{cases} cases, {bad} failures, worst A2 {worst:.2e}, {time.time() - t0:.0f} s")
+    return 1 if bad else 0
+
+
+if __name__ == "__main__":
+    sys.exit(main(int(sys.argv[1]) if len(sys.argv) > 1 else 40, int(sys.argv[2]) if len(sys.argv) > 2 else 0))

@@ -165,3 +165,31 @@ def test_euler_merged_block_on_host(tmp_path, bits, dagger):
         ref = np.einsum("ij,qxjy->qxiy", A, t).reshape(nvec, 1 << R)
     for q in range(nvec):
         np.testing.assert_allclose(got[q] / P.sc[q], ref[q], atol=2e-5)
+
+
+@pytest.mark.parametrize("seed", [3, 7])
+def test_kernels_generate_for_random_hardware_style_circuits(seed):
+    """Kernel generation (no compile) over the randomised IBM / IonQ / VQ-style circuits of the
+    GPU stress run (profiles/stress_structured.py), with the engine's compile settings. Seed 3
+    holds the case that broke the merged Euler runs on the GPU box: ECR applied twice on one pair
+    is an identity permutation that emits no op, so two groups of one wire become neighbours."""
+    import importlib.util
+    import os
+
+    from paper_2506_04891_b200.engine import forward_program
+
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "stress_structured.py")
+    spec = importlib.util.spec_from_file_location("stress_structured", path)
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    mod.rng = np.random.default_rng(seed)
+    kw = dict(prefix=True, fold=True, split=True)
+    for _ in range(14):
+        fam, circ, n, M, B = mod.draw_case()
+        mod.rng.uniform(-3, 3, circ.trainable_count)  # keep the stress run's draw order
+        mod.rng.uniform(0, 3, (B, circ.encoding_count))
+        mod.rng.normal(size=n)
+        prog = S.compile_circuit(circ, M=M, R=S.DEFAULT_R_SPECIALISED if M >= 9 else S.default_r(M), **kw)
+        pf = forward_program(circ, prog, M=M, isolate=(), direct=(), split_layers=(), **kw)
+        ks = codegen.kernel_set(prog, pf)
+        assert len(ks) == 2 * len(prog.passes)
