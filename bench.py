@@ -621,7 +621,8 @@ def run_ours(args, world, rank, local):
         eng = _engine(wl.circuit, plan, dev)
     else:
         eng = Engine(wl.circuit, device=dev, M=args.M, R=args.R, isolate=sel(KernelKind.ISOLATED),
-                     direct=sel(KernelKind.DIRECT), split_layers=sel(KernelKind.SPLIT))
+                     direct=sel(KernelKind.DIRECT), split_layers=sel(KernelKind.SPLIT),
+                     rebalance_budget=plan.rebalance_budget)
     ck = None if args.checkpoint is None else bool(args.checkpoint)
     gate = None
     if args.batch is None:  # BASELINE workloads only (golden rows are the first rows of the batch)
@@ -795,6 +796,7 @@ def run_ours(args, world, rank, local):
                    "passes": len(eng.program.passes), "tile_bits": eng.program.passes[0].M,
                    "tile_bits_choice": tile_choice, "plan": plan_src,
                    "plan_variants": {k.value: sum(1 for x in kinds if x is k) for k in set(kinds)},
+                   "rebalance_budget": plan.rebalance_budget,
                    "cuda_graph": gstep.graph is not None,
                    "reg_bits": eng.program.passes[0].R, "variant": eng.variant,
                    "l2": f"working set {2 * b * (8 << n) / 2**20:.0f} MiB (psi+lambda) vs 126 MB L2"

@@ -176,7 +176,8 @@ class Engine:
     """A circuit compiled for the device; the object behind the drop-in API."""
 
     def __init__(self, circuit, M: int | None = None, R: int | None = None, device=None, jit=None,
-                 isolate=(), prefix=None, fold=None, split=None, direct=(), split_layers=()):
+                 isolate=(), prefix=None, fold=None, split=None, direct=(), split_layers=(),
+                 rebalance_budget=None):
         self.device = torch.device(device if device is not None else "cuda")
         if self.device.type != "cuda":
             raise ValueError("the engine runs on CUDA devices only")
@@ -201,7 +202,8 @@ class Engine:
         # diagonal gates split out of one-qubit groups when the remainder is cheaper
         if split is None:
             split = os.environ.get("LSQ_SPLIT", "1") != "0"
-        kw = dict(isolate=isolate, prefix=prefix, fold=fold, split=split, direct=direct, split_layers=split_layers)
+        kw = dict(isolate=isolate, prefix=prefix, fold=fold, split=split, direct=direct, split_layers=split_layers,
+                  rebalance_budget=rebalance_budget)
         self.program = compile_circuit(circuit, M=M, R=R, **kw)
         self.program_fwd = forward_program(circuit, self.program, M=M, **kw)
         self.prefix = bool(self.program.prefix) or bool(self.program.obs)
@@ -544,7 +546,7 @@ _CACHE_MAX = 8  # engines (programs + held state buffers) kept alive, least rece
 
 
 def engine_for(circuit, device=None, M=None, R=None, jit=None, isolate=(), prefix=None, direct=(),
-               split_layers=()) -> Engine:
+               split_layers=(), rebalance_budget=None) -> Engine:
     """Cached Engine per (circuit layers, n, tiling, variant, device)."""
     dev = torch.device(device if device is not None else "cuda")
     if dev.type == "cuda" and dev.index is None:
@@ -557,11 +559,11 @@ def engine_for(circuit, device=None, M=None, R=None, jit=None, isolate=(), prefi
     isolate = tuple(sorted(set(int(i) for i in isolate)))
     direct = tuple(sorted(set(int(i) for i in direct)))
     split_layers = tuple(sorted(set(int(i) for i in split_layers)))
-    key = (_circuit_key(circuit), M, R, jit, isolate, prefix, direct, split_layers, str(dev))
+    key = (_circuit_key(circuit), M, R, jit, isolate, prefix, direct, split_layers, rebalance_budget, str(dev))
     eng = _CACHE.get(key)
     if eng is None:
         eng = Engine(circuit, M=M, R=R, device=dev, jit=jit, isolate=isolate, prefix=prefix, direct=direct,
-                     split_layers=split_layers)
+                     split_layers=split_layers, rebalance_budget=rebalance_budget)
         _CACHE[key] = eng
         while len(_CACHE) > _CACHE_MAX:
             _CACHE.popitem(last=False)

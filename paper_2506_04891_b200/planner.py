@@ -104,6 +104,7 @@ class Plan:
     assignments: tuple
     measurements: tuple
     tile_bits: int | None = None
+    rebalance_budget: float | None = None  # pass-rebalancing budget measured best (None: default)
 
 
 def tiling_of(plan, circuit):
@@ -121,6 +122,9 @@ def layer_signature(layer, n: int) -> tuple:
 
 
 TILE_BITS_CANDIDATES = (10, 11, 12, 13)
+# pass-rebalancing budgets (estimated packed FP32 ops per amplitude a pass may reach by taking
+# groups from the pass before it, schedule.rebalance_passes) tried by build_plan
+REBALANCE_CANDIDATES = (40.0, 120.0, 220.0)
 
 
 def _draw(circuit, batch, seed):
@@ -132,7 +136,7 @@ def _draw(circuit, batch, seed):
 
 def time_program(circuit, batch: int, objective: "Objective" = None, M=None, isolate=(), reps: int = 10,
                  warmup: int = 3, timer=None, seed: int = 0, device=None, direct=(),
-                 split_layers=()) -> TimingStats:
+                 split_layers=(), rebalance_budget=None) -> TimingStats:
     """Time the whole compiled program (one CUDA variant) with the reference's protocol:
     `warmup` untimed runs then `reps` timed runs (reference planner.py:106-162). Default clock:
     CUDA events on the engine's stream; an injected `timer` is called around each rep after
@@ -147,7 +151,7 @@ def time_program(circuit, batch: int, objective: "Objective" = None, M=None, iso
     if warmup < 0:
         raise ValueError("warmup cannot be negative")
     eng = Engine(circuit, M=M, isolate=isolate, device=device, direct=direct, split_layers=split_layers,
-                 fold=False if objective is Objective.FORWARD else None)
+                 fold=False if objective is Objective.FORWARD else None, rebalance_budget=rebalance_budget)
     th, x = _draw(circuit, batch, seed)
     th_d = None if th is None else torch.as_tensor(th, device=eng.device)
     x_d = None if x is None else torch.as_tensor(x, device=eng.device)
@@ -187,6 +191,9 @@ def build_plan(circuit, batch: int, objective: "Objective" = None, timer=None, r
     2. per layer signature, in order of first appearance: every applicable variant (ISOLATED,
        DIRECT, SPLIT) is timed on the whole program with the variants kept so far; the fastest
        is kept for all layers of the signature (ties -> declaration order, FUSED first).
+    3. the pass-rebalancing budget: every candidate of REBALANCE_CANDIDATES is timed on the
+       whole program with the kept variants; argmin (real timing only: an injected `measure`
+       leaves the default budget).
 
     `measure(layer, kernel) -> TimingStats` replaces real timing (tests): it is asked for the
     per-layer variants, and `measure(None, M)` for tile exponents.
@@ -195,11 +202,11 @@ def build_plan(circuit, batch: int, objective: "Objective" = None, timer=None, r
     n = int(circuit.n)
     layers = list(circuit.layers)
 
-    def timed(M, assign):
+    def timed(M, assign, budget=None):
         sel = lambda kk: sorted(i for i, k in assign.items() if k is kk)  # noqa: E731
         return time_program(circuit, batch, objective, M=M, isolate=sel(KernelKind.ISOLATED), reps=reps,
                             warmup=warmup, timer=timer, seed=seed, direct=sel(KernelKind.DIRECT),
-                            split_layers=sel(KernelKind.SPLIT))
+                            split_layers=sel(KernelKind.SPLIT), rebalance_budget=budget)
 
     if tile_bits is None:
         cands = sorted({min(n, m) for m in TILE_BITS_CANDIDATES})
@@ -234,7 +241,13 @@ def build_plan(circuit, batch: int, objective: "Objective" = None, timer=None, r
         assignments[idx] = best
         for k, st in stats.items():
             measurements.append(PlanMeasurement(idx, k, st.mean_seconds, st.std_seconds, st.reps))
-    return Plan(machine_id(), n, batch, objective, tuple(assignments), tuple(measurements), tile_bits)
+    budget = None
+    if measure is None and objective is Objective.FORWARD_BACKWARD:
+        from .schedule import REBALANCE_BUDGET
+
+        stats_b = {b: (base if b == REBALANCE_BUDGET else timed(tile_bits, chosen, b)) for b in REBALANCE_CANDIDATES}
+        budget = min(stats_b, key=lambda b: (stats_b[b].mean_seconds, b))
+    return Plan(machine_id(), n, batch, objective, tuple(assignments), tuple(measurements), tile_bits, budget)
 
 
 def choose_tile_bits(circuit, batch: int, objective: "Objective" = None, candidates=TILE_BITS_CANDIDATES,
@@ -281,6 +294,7 @@ def serialize_plan(plan: Plan) -> str:
         "batch": plan.batch,
         "objective": plan.objective.value,
         "tile_bits": plan.tile_bits,
+        "rebalance_budget": plan.rebalance_budget,
         "assignments": [{"layer_index": i, "kernel": k.value} for i, k in enumerate(plan.assignments)],
         "measurements": [
             {"layer_index": m.layer_index, "kernel": m.kernel.value, "mean_s": m.mean_s,
@@ -316,10 +330,12 @@ def parse_plan(text: str) -> Plan:
                             float(_req(it, "mean_s", w)), float(_req(it, "std_s", w)), int(_req(it, "reps", w)))
         )
     tb = doc.get("tile_bits")
+    rb = doc.get("rebalance_budget")
     return Plan(
         str(_req(doc, "machine_id", "document")), int(_req(doc, "n", "document")),
         int(_req(doc, "batch", "document")), Objective(_req(doc, "objective", "document")),
         tuple(k for _, k in pairs), tuple(meas), None if tb is None else int(tb),
+        None if rb is None else float(rb),
     )
 
 

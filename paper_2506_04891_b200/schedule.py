@@ -482,7 +482,7 @@ REBALANCE_BUDGET = float(_os.environ.get("LSQ_REBALANCE_BUDGET", "40"))
 REBALANCE = _os.environ.get("LSQ_REBALANCE", "1") != "0"
 
 
-def rebalance_passes(passes: list[PassPlan], groups, n: int) -> None:
+def rebalance_passes(passes: list[PassPlan], groups, n: int, budget: float | None = None) -> None:
     """Move work from heavy passes into the light ones after them (in place). The greedy
     partition packs each pass as full as its tile allows, so the last passes of a circuit carry
     little FP32 work and run at the HBM roofline with the FMA pipe mostly idle (cfg4's last two
@@ -493,6 +493,7 @@ def rebalance_passes(passes: list[PassPlan], groups, n: int) -> None:
     unchanged (dependencies stay ordered; gids are a topological order)."""
     if len(passes) < 2:
         return
+    budget = REBALANCE_BUDGET if budget is None else float(budget)
     succ = [set() for _ in groups]
     for g in groups:
         for p_ in group_preds(groups)[g.gid]:
@@ -502,7 +503,7 @@ def rebalance_passes(passes: list[PassPlan], groups, n: int) -> None:
         dst, src = passes[i], passes[i - 1]
         load = sum(_fp_cost(groups[x]) for x in dst.groups)
         moved = True
-        while moved and load < REBALANCE_BUDGET:
+        while moved and load < budget:
             moved = False
             for gid in sorted(src.groups, reverse=True):
                 g = groups[gid]
@@ -511,7 +512,7 @@ def rebalance_passes(passes: list[PassPlan], groups, n: int) -> None:
                 if not g.diag and not set(g.wires) <= dst.tile_wires:
                     continue
                 c = _fp_cost(g)
-                if load + c > REBALANCE_BUDGET:
+                if load + c > budget:
                     continue
                 src.groups.remove(gid)
                 dst.groups = sorted(dst.groups + [gid])
@@ -855,7 +856,7 @@ def observable_masks(perms, n: int):
 
 def compile_circuit(circuit, M: int | None = None, R: int | None = None, isolate=(),
                     prefix: bool = False, fold: bool = False, split: bool = False, direct=(),
-                    split_layers=(), fwd_only: bool = False) -> Program:
+                    split_layers=(), fwd_only: bool = False, rebalance_budget: float | None = None) -> Program:
     """Compile a (reference-compatible) circuit into a pass program.
 
     Planner variants (layer indices): `isolate` -- executed with pass boundaries of their own
@@ -865,6 +866,9 @@ def compile_circuit(circuit, M: int | None = None, R: int | None = None, isolate
     gate of these (diagonal) layers are split into diagonal runs and the rest (SPLIT).
     `fwd_only`: the program only provides forward kernels (engine.forward_program), so the phase
     search prefers plans whose LAST phase keeps the coalescing bits on lanes (forward stores).
+    `rebalance_budget`: estimated FP32 load (packed ops per amplitude) up to which a pass takes
+    groups from the pass before it (rebalance_passes); None = REBALANCE_BUDGET. A plan carries the
+    value the planner measured best for its circuit.
     """
     n = int(circuit.n)
     gates = flatten_gates(circuit)
@@ -905,7 +909,7 @@ def compile_circuit(circuit, M: int | None = None, R: int | None = None, isolate
                 grp[gid].trailing = True
         seg_passes = schedule_passes(grp, n, M, skip=skip) if (grp or not passes) else []
         if REBALANCE and not (prefix and si == 0 and len(segs) > 1):
-            rebalance_passes(seg_passes, grp, n)
+            rebalance_passes(seg_passes, grp, n, rebalance_budget)
         need2 = any(g.arity == 2 and not g.diag for g in grp)
         for pp in seg_passes:
             r = default_r(pp.M) if R is None else min(R, pp.M)
@@ -944,6 +948,7 @@ def compile_circuit(circuit, M: int | None = None, R: int | None = None, isolate
     prog.isolate = tuple(sorted(iso))
     prog.direct_layers = frozenset(int(i) for i in direct)
     prog.split_layers = tuple(sorted(int(i) for i in split_layers))
+    prog.rebalance_budget = rebalance_budget
     prog.prefix = {w: gid for w, gid in pre.items()}
     prog.obs = obs
     prog.drop_phase = bool(fold)  # gradient program: global phases of constant groups dropped

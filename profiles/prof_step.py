@@ -26,7 +26,8 @@ if M is None and os.path.exists(plan_path):
     kinds = plan_kernels(wl.circuit, plan)
     sel = lambda kk: [i for i, k in enumerate(kinds) if k is kk]  # noqa: E731
     M = plan.tile_bits
-    kw = dict(isolate=sel(KernelKind.ISOLATED), direct=sel(KernelKind.DIRECT), split_layers=sel(KernelKind.SPLIT))
+    kw = dict(isolate=sel(KernelKind.ISOLATED), direct=sel(KernelKind.DIRECT), split_layers=sel(KernelKind.SPLIT),
+              rebalance_budget=plan.rebalance_budget)
 eng = Engine(wl.circuit, M=M, R=R, **kw)
 th = torch.as_tensor(wl.theta, device="cuda"); x = torch.as_tensor(wl.x, device="cuda")
 w = torch.as_tensor(wl.weights, device="cuda")

@@ -18,7 +18,7 @@ from paper_2506_04891_b200.core import plan_kernels
 from paper_2506_04891_b200.schedule import compile_circuit
 wl=make_workload($1, batch=1); p=load_plan('profiles/plans/cfg$1.json'); k=plan_kernels(wl.circuit,p)
 s=lambda kk:[i for i,x in enumerate(k) if x is kk]
-prog=compile_circuit(wl.circuit,M=p.tile_bits,R=4,isolate=s(KernelKind.ISOLATED),prefix=True,fold=True,split=True,direct=s(KernelKind.DIRECT),split_layers=s(KernelKind.SPLIT))
+prog=compile_circuit(wl.circuit,M=p.tile_bits,R=4,isolate=s(KernelKind.ISOLATED),prefix=True,fold=True,split=True,direct=s(KernelKind.DIRECT),split_layers=s(KernelKind.SPLIT),rebalance_budget=p.rebalance_budget)
 print(2*len(prog.passes)-1, p.tile_bits)"; }
 for spec in "4 0 1" "3 0 1" "5 39 1"; do
   set -- $spec; C=$1; B=$2; SC=$3

@@ -102,8 +102,15 @@ def test_plan_json_roundtrip_and_errors(tmp_path):
     plan = P.build_plan(c, 2, P.Objective.FORWARD_BACKWARD, measure=_table(iso_faster=("cnot",)))
     again = P.plan_roundtrip(plan)
     assert again == plan
+    assert plan.rebalance_budget is None  # an injected measure leaves the default budget
     doc = json.loads(P.serialize_plan(plan))
     assert set(doc) >= {"machine_id", "n", "batch", "objective", "assignments", "measurements", "tile_bits"}
+    # the measured pass-rebalancing budget travels with the plan; plans without one still parse
+    import dataclasses
+
+    with_b = dataclasses.replace(plan, rebalance_budget=160.0)
+    assert P.plan_roundtrip(with_b) == with_b and P.plan_roundtrip(with_b).rebalance_budget == 160.0
+    assert P.parse_plan(json.dumps({k: v for k, v in doc.items() if k != "rebalance_budget"})).rebalance_budget is None
     with pytest.raises(ValueError):
         P.parse_plan(json.dumps({k: v for k, v in doc.items() if k != "n"}))
     bad = dict(doc)

@@ -240,3 +240,18 @@ def test_all_variants_compile_and_emulate(cfg):
     res = Emulator(prog).gradient(wl.theta, wl.x, 2, wl.weights)
     ref = orc.gradient(wl.circuit, wl.theta, wl.x, batch=2, weights=wl.weights)
     _cmp(res, ref, atol=1e-8)
+
+
+def test_rebalance_budget_moves_groups_and_keeps_semantics():
+    """A larger pass-rebalancing budget moves groups into later passes (cfg4-shaped circuit) and
+    the program still matches the oracle on the emulator."""
+    wl = make_workload(4, n=12, batch=1)
+    a = S.compile_circuit(wl.circuit, M=8, R=4, prefix=True, fold=True, split=True, rebalance_budget=0.0)
+    b = S.compile_circuit(wl.circuit, M=8, R=4, prefix=True, fold=True, split=True, rebalance_budget=400.0)
+    assert [sorted(p.groups) for p in a.passes] != [sorted(p.groups) for p in b.passes]
+    assert sorted(g for p in b.passes for g in p.groups) == sorted(g for p in a.passes for g in p.groups)
+    wl = make_workload(4, n=7, batch=2)
+    ref = orc.gradient(wl.circuit, wl.theta, wl.x, batch=2, weights=wl.weights)
+    for budget in (0.0, 60.0, 400.0):
+        prog = S.compile_circuit(wl.circuit, M=4, R=2, prefix=True, fold=True, split=True, rebalance_budget=budget)
+        _cmp(Emulator(prog).gradient(wl.theta, wl.x, 2, wl.weights), ref, atol=1e-8)
