@@ -23,4 +23,4 @@ for cfg in [int(a) for a in sys.argv[1:]] or [4, 3, 2, 5]:
     kinds = {}
     for k in plan.assignments:
         kinds[k.value] = kinds.get(k.value, 0) + 1
-    print(f"cfg{cfg}: M={plan.tile_bits} {kinds} on {rows} rows in {time.time() - t0:.0f} s -> {path}", flush=True)
+    print(f"cfg{cfg}: M={plan.tile_bits} rebalance_budget={plan.rebalance_budget} {kinds} on {rows} rows in {time.time() - t0:.0f} s -> {path}", flush=True)
