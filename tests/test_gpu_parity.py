@@ -357,11 +357,27 @@ def test_build_plan_real_timing_and_replay():
     wl = make_workload(4, n=13, batch=4)
     plan = P.build_plan(wl.circuit, 4, P.Objective.FORWARD_BACKWARD, reps=2, warmup=1)
     assert plan.tile_bits in (10, 11, 12, 13)
+    assert plan.rebalance_budget in P.REBALANCE_CANDIDATES  # measured (real timing)
     assert len(plan.assignments) == len(wl.circuit.layers)
     a = gradient(wl.circuit, wl.theta, wl.x, batch=4, weights=wl.weights, plan=plan)
     b = gradient(wl.circuit, wl.theta, wl.x, batch=4, weights=wl.weights)
     np.testing.assert_allclose(a.zq, b.zq, atol=1e-6)
     assert_grads_close(a.grads, b.grads)
+
+
+@pytest.mark.parametrize("cfg,budget", [(4, 220.0), (5, 120.0), (2, 220.0)])
+def test_plan_rebalance_budget_vs_oracle(cfg, budget):
+    """A plan's pass-rebalancing budget (groups moved into later passes) replayed through the public
+    gradient() on a multi-pass program against the oracle."""
+    import dataclasses
+
+    from paper_2506_04891_b200 import planner as P
+
+    wl = make_workload(cfg, n=14, batch=3)
+    plan = dataclasses.replace(P.plan_for_tile_bits(wl.circuit, 3, 10), rebalance_budget=budget)
+    res = gradient(wl.circuit, wl.theta, wl.x, batch=3, weights=wl.weights, plan=plan)
+    ref = orc.gradient(wl.circuit, wl.theta, wl.x, batch=3, weights=wl.weights)
+    check(res, ref, what=f"cfg{cfg}_budget{int(budget)}")
 
 
 @pytest.mark.parametrize("cfg,n", [(4, 12), (3, 12), (5, 12), (2, 12)])
