@@ -696,7 +696,8 @@ def run_ours(args, world, rank, local):
             mode, pidx = divmod(kind, 1000)
             vec = _pass_vectors(eng.program, mode, pidx, eng.last_adjoint)
             key = _kernel_label(eng, mode, pidx)
-            d = per_kernel.setdefault(key, {"bytes": 0.0, "ms": 0.0, "launches": 0})
+            d = per_kernel.setdefault(key, {"bytes": 0.0, "ms": 0.0, "launches": 0, "rows": 0})
+            d["rows"] += rows_launch
             d["bytes"] += vec * rows_launch * (8 << n)
             d["ms"] += t
             d["launches"] += 1
@@ -718,7 +719,11 @@ def run_ours(args, world, rank, local):
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get(f"{CONFIG_NAMES[cfg]}|{dom[0]}")
+            tab = json.load(open(prof))
+            traffic = tab.get(f"{CONFIG_NAMES[cfg]}|{dom[0]}")
+            cap_rows = tab.get(f"{CONFIG_NAMES[cfg]}|rows")  # rows per launch of the ncu capture
+            if traffic is not None and cap_rows:
+                traffic = round(traffic * (dom[1]["rows"] / dom[1]["launches"]) / cap_rows)
         except Exception:
             traffic = None
     roofline = {

@@ -1,7 +1,8 @@
 """DRAM traffic per launch (dram__bytes_read.sum + dram__bytes_write.sum, from an
 `ncu --set full` capture) per JIT kernel family, recorded for bench.py's roofline "traffic".
-usage: python profiles/ncu_traffic.py REPORT.ncu-rep WORKLOAD_NAME M [ROWS_SCALE]
-ROWS_SCALE rescales a capture taken on fewer rows than the bench's launches (default 1)."""
+usage: python profiles/ncu_traffic.py REPORT.ncu-rep WORKLOAD_NAME M [ROWS_SCALE] [ROWS]
+ROWS_SCALE rescales the captured bytes (default 1); ROWS = rows per launch of the capture, recorded
+as "<workload>|rows" so bench.py scales the figure to its own rows per launch (micro-batches)."""
 import json
 import os
 import re
@@ -12,6 +13,7 @@ from ncu_summary import load  # noqa: E402
 
 rep, workload, M = sys.argv[1], sys.argv[2], int(sys.argv[3])
 scale = float(sys.argv[4]) if len(sys.argv) > 4 else 1.0
+cap_rows = int(sys.argv[5]) if len(sys.argv) > 5 else None
 names = {0: "forward", 1: "turnaround", 2: "adjoint"}
 fam: dict = {}
 for k in load(rep):
@@ -26,4 +28,6 @@ data = json.load(open(out_path)) if os.path.exists(out_path) else {}
 for label, v in fam.items():
     data[f"{workload}|{label}"] = round(sum(v) / len(v))
     print(workload, label, len(v), "launches, mean bytes/launch", round(sum(v) / len(v)))
+if cap_rows:
+    data[f"{workload}|rows"] = cap_rows
 json.dump(data, open(out_path, "w"), indent=1, sort_keys=True)

@@ -20,13 +20,13 @@ wl=make_workload($1, batch=1); p=load_plan('profiles/plans/cfg$1.json'); k=plan_
 s=lambda kk:[i for i,x in enumerate(k) if x is kk]
 prog=compile_circuit(wl.circuit,M=p.tile_bits,R=4,isolate=s(KernelKind.ISOLATED),prefix=True,fold=True,split=True,direct=s(KernelKind.DIRECT),split_layers=s(KernelKind.SPLIT),rebalance_budget=p.rebalance_budget)
 print(2*len(prog.passes)-1, p.tile_bits)"; }
-for spec in "4 0 1" "3 0 1" "5 39 1"; do
-  set -- $spec; C=$1; B=$2; SC=$3
+for spec in "4 0 1 256" "3 0 1 128" "5 39 1 39"; do
+  set -- $spec; C=$1; B=$2; SC=$3; ROWS=$4
   read K M <<< "$(passes $C)"
   timeout 1200 ncu --set full --clock-control none --import-source on -k 'regex:lsq_jit_p' -c $K -f -o /tmp/full_c${C} \
      python profiles/prof_step.py $C 1 $B > gpurun_out/ncu_full_c${C}_$T.log 2>&1; echo "ncu full cfg$C rc=$? K=$K M=$M"
   python profiles/ncu_summary.py /tmp/full_c${C}.ncu-rep --json gpurun_out/ncu_full_c${C}_$T.json > gpurun_out/ncu_full_c${C}_$T.txt 2>&1
-  python profiles/ncu_traffic.py /tmp/full_c${C}.ncu-rep $(python -c "from paper_2506_04891_b200.configs import CONFIG_NAMES; print(CONFIG_NAMES[$C])") $M $SC >> gpurun_out/ncu_traffic_$T.log 2>&1
+  python profiles/ncu_traffic.py /tmp/full_c${C}.ncu-rep $(python -c "from paper_2506_04891_b200.configs import CONFIG_NAMES; print(CONFIG_NAMES[$C])") $M $SC $ROWS >> gpurun_out/ncu_traffic_$T.log 2>&1
 done
 cp profiles/ncu_traffic.json gpurun_out/ncu_traffic.json
 rm -f gpurun_out/ncu_fp32.json
