@@ -1217,6 +1217,7 @@ def _emit_ops(w, P, ph_idx, mode_bwd, nv):
                 for q in range(nv if mode_bwd else 1):
                     _emit_unit_const(w, P, f"v[{q}]", V, bits, mode_bwd)
                     P.sc[q] /= kappa
+                _guard_scale(w, P, nv if mode_bwd else 1)  # deep single-pass circuits: fp32 range
             elif U is not None:
                 for q in range(nv):
                     _emit_const_u(w, P, f"v[{q}]", U, bits, mode_bwd)

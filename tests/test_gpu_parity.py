@@ -33,7 +33,7 @@ if not torch.cuda.is_available():  # pragma: no cover
 
 from oracle import layersim_oracle as orc  # noqa: E402
 from paper_2506_04891_b200 import gradient, apply_circuit, backward_sweep  # noqa: E402
-from paper_2506_04891_b200.circuits import Circuit, Layer, all_qubits, explicit, ring_pairs  # noqa: E402
+from paper_2506_04891_b200.circuits import Circuit, Layer, Role, all_qubits, explicit, ring_pairs  # noqa: E402
 from paper_2506_04891_b200.configs import make_workload  # noqa: E402
 from paper_2506_04891_b200.engine import Engine  # noqa: E402
 from paper_2506_04891_b200.gates import GateKind  # noqa: E402
@@ -424,6 +424,35 @@ def test_compiler_knobs_vs_oracle(cfg, n, knobs, monkeypatch):
     np.testing.assert_allclose(r["zq"].cpu().numpy(), ref["zq"], atol=Z_TOL)
     assert_grads_close(_angles(r["grads"].cpu().numpy(), r["encoding_grads"].cpu().numpy()),
                        _angles(ref["grads"], ref["encoding_grads"]), what=f"cfg{cfg}_knobs")
+
+
+@pytest.mark.parametrize("gate2,blocks", [("ecr", 60), ("ms", 40)])
+def test_deep_single_pass_circuit_scale_guard(gate2, blocks):
+    """A deep circuit that runs as ONE on-chip pass (n=10): hundreds of unit-form constant gates and
+    Euler-form groups defer a compile-time scale of 2^(ops/2), which must be folded back into the
+    amplitudes before it leaves the fp32 range (codegen._guard_scale)."""
+    n = 10
+    ev = explicit(*[(q, q + 1) for q in range(0, n - 1, 2)])
+    od = explicit(*[(q, q + 1) for q in range(1, n - 1, 2)])
+    layers = [Layer(GateKind("ry"), all_qubits(), Role.ENCODING)]
+    for _ in range(blocks):
+        if gate2 == "ecr":
+            layers += [Layer(GateKind("rz"), all_qubits(), Role.TRAINABLE), Layer(GateKind("sx"), all_qubits()),
+                       Layer(GateKind("rz"), all_qubits(), Role.TRAINABLE)]
+            layers += [Layer(GateKind("ecr"), ev), Layer(GateKind("ecr"), od)]
+        else:
+            layers += [Layer(GateKind("gpi2"), all_qubits(), Role.TRAINABLE), Layer(GateKind("gpi"), all_qubits(), Role.TRAINABLE)]
+            layers += [Layer(GateKind("ms"), p, Role.FIXED, [[0.0, 0.0, 0.25]] * len(p.wires)) for p in (ev, od)]
+    circ = Circuit(n, layers)
+    rng = np.random.default_rng(5)
+    theta = rng.uniform(-3, 3, circ.trainable_count)
+    x = rng.uniform(0, 3, (2, circ.encoding_count))
+    w = rng.normal(size=n)
+    res = gradient(circ, theta, x, batch=2, weights=w)
+    assert np.all(np.isfinite(res.zq)) and np.all(np.isfinite(res.grads))
+    ref = orc.gradient(circ, theta, x, batch=2, weights=w)
+    tol, note = precision_model_tol(circ, theta, x, w, ref, 2)
+    check(res, ref, tol=tol, note=note, what=f"deep_{gate2}")
 
 
 def test_choose_tile_bits_and_plan_replay():
