@@ -902,6 +902,10 @@ def compile_circuit(circuit, M: int | None = None, R: int | None = None, isolate
             skip |= set(pre.values())
         if fold and si == len(segs) - 1:
             tr, perms = trailing_groups(grp)
+            # a permutation group that is also its wire's product-state prefix (e.g. SX.SX = X on
+            # a wire only permutations touch afterwards) is synthesized, not folded: it must not
+            # flip the observable a second time
+            perms = [g for g in perms if g.gid not in skip]
             tr = [g for g in tr if g not in skip]
             skip |= set(tr)
             obs = observable_masks(perms, n)

@@ -255,3 +255,25 @@ def test_rebalance_budget_moves_groups_and_keeps_semantics():
     for budget in (0.0, 60.0, 400.0):
         prog = S.compile_circuit(wl.circuit, M=4, R=2, prefix=True, fold=True, split=True, rebalance_budget=budget)
         _cmp(Emulator(prog).gradient(wl.theta, wl.x, 2, wl.weights), ref, atol=1e-8)
+
+
+def test_prefix_group_that_is_also_a_trailing_permutation():
+    """SX.SX = X on wires that only permutations / diagonals touch afterwards is both the wire's
+    product-state prefix and a trailing permutation: it is synthesized, and must not flip the
+    folded observable as well (found by profiles/stress_random.py on the GPU: <Z> off by 2)."""
+    from paper_2506_04891_b200.circuits import Circuit, Layer, Role, all_qubits, explicit, ring_pairs
+    from paper_2506_04891_b200.gates import GateKind
+
+    n = 6
+    circ = Circuit(n, [Layer(GateKind("sx"), all_qubits()), Layer(GateKind("sx"), all_qubits()),
+                       Layer(GateKind("ms"), explicit((4, 1), (0, 1), (2, 3)), Role.TRAINABLE),
+                       Layer(GateKind("cnot"), ring_pairs()), Layer(GateKind("swap"), explicit((0, 4), (5, 1))),
+                       Layer(GateKind("cz"), ring_pairs())])
+    rng = np.random.default_rng(3)
+    theta = rng.uniform(-3, 3, circ.trainable_count)
+    w = rng.normal(size=n)
+    ref = orc.gradient(circ, theta, None, batch=2, weights=w)
+    for M in (4, 6):
+        prog = S.compile_circuit(circ, M=M, R=2, prefix=True, fold=True, split=True)
+        assert any(g.prefix and g.perm_ops is not None for g in prog.groups)
+        _cmp(Emulator(prog).gradient(theta, None, 2, w), ref, atol=1e-8)
