@@ -2,7 +2,8 @@
 tests/circuit_helpers.py) at random widths and tilings; the numpy oracle is the checker. Bound per
 case: <Z_q> 1e-5 absolute; gradients A2 at 1e-4, or twice the A2 error of the reference algorithm
 run in complex64 where that precision model itself breaks 1e-4 (the rule of
-tests/test_gpu_parity.py::test_random_circuits_multipass); structurally zero gradients absolutely.
+tests/test_gpu_parity.py::test_random_circuits_multipass); structurally zero gradients absolutely
+(1e-6, or twice the complex64 model's own noise on them).
 usage: python profiles/stress_random.py [CASES] [SEED]"""
 import os
 import sys
@@ -44,7 +45,11 @@ def main(cases, seed):
         gr = np.concatenate([ref["grads"], ref["encoding_grads"]], 1)
         zerr = float(np.abs(r["zq"].cpu().numpy() - ref["zq"]).max())
         if gr.size and np.abs(gr).max() < 1e-12:
+            # structurally zero gradients: absolute, against the complex64 model's own noise
             err, tol = float(np.abs(g).max()), 1e-6
+            if err > tol:
+                r32 = orc.gradient(circ, theta, x, batch=B, weights=w, dtype=np.complex64)
+                tol = max(tol, 2 * float(np.abs(np.concatenate([r32["grads"], r32["encoding_grads"]], 1)).max()))
         else:
             err, tol = a2(g, gr), 1e-4
             if err > tol:  # the precision model decides
