@@ -277,3 +277,31 @@ def test_prefix_group_that_is_also_a_trailing_permutation():
         prog = S.compile_circuit(circ, M=M, R=2, prefix=True, fold=True, split=True)
         assert any(g.prefix and g.perm_ops is not None for g in prog.groups)
         _cmp(Emulator(prog).gradient(theta, None, 2, w), ref, atol=1e-8)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_random_all_gate_circuits_on_the_emulator(seed):
+    """The draw sequence of the GPU stress run (profiles/stress_random.py) on the CPU: random
+    circuits of all gate kinds, widths and tilings compiled like the engine does and interpreted
+    by the emulator against the oracle (the narrow ones; seed 0 holds the case whose folded
+    observable was flipped twice)."""
+    from circuit_helpers import random_circuit
+
+    rng = np.random.default_rng(seed)
+    checked = 0
+    for _ in range(70):
+        n = int(rng.integers(6, 13))
+        M = int(rng.integers(5, n + 1))
+        circ = random_circuit(rng, n, int(rng.integers(6, 18)))
+        B = int(rng.integers(1, 4))
+        theta = rng.uniform(-3, 3, circ.trainable_count)
+        x = rng.uniform(0, 3, (B, circ.encoding_count))
+        w = rng.normal(size=n)
+        if n > 8:
+            continue
+        m = min(n, M)
+        prog = S.compile_circuit(circ, M=M, R=S.DEFAULT_R_SPECIALISED if m >= 9 else S.default_r(m),
+                                 prefix=True, fold=True, split=True)
+        _cmp(Emulator(prog).gradient(theta, x, B, w), orc.gradient(circ, theta, x, batch=B, weights=w), atol=1e-7)
+        checked += 1
+    assert checked >= 20
