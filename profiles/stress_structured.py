@@ -112,11 +112,18 @@ def main(cases, seed):
             a2 = float(np.max(np.abs(g - gr) / np.maximum(np.abs(gr), 1e-2 * np.abs(gr).max())))
         else:  # structurally zero gradients: absolute
             a2 = float(np.abs(g).max())
-        ok = zerr <= 1e-5 and a2 <= 1e-4
+        tol = 1e-4
+        if a2 > tol and gr.size and np.abs(gr).max() > 1e-9:
+            # the rule of the random-circuit tests: twice the A2 error of the reference algorithm
+            # run in complex64 where that precision model itself breaks 1e-4 (tiny gradients)
+            r32 = orc.gradient(circ, theta, x, batch=B, weights=w, dtype=np.complex64)
+            g32 = np.concatenate([r32["grads"], r32["encoding_grads"]], 1)
+            tol = max(tol, 2 * float(np.max(np.abs(g32 - gr) / np.maximum(np.abs(gr), 1e-2 * np.abs(gr).max()))))
+        ok = zerr <= 1e-5 and a2 <= tol
         worst = max(worst, a2)
         bad += not ok
         print(f"case {c:3d} {fam:4s} n={n:2d} M={M:2d} B={B} layers={len(circ.layers):2d} passes={len(eng.program.passes):2d} "
-              f"phases={sum(len(p.phases) for p in eng.program.passes):3d} zq_err={zerr:.1e} a2={a2:.1e} {'ok' if ok else 'FAIL'}",
+              f"phases={sum(len(p.phases) for p in eng.program.passes):3d} zq_err={zerr:.1e} a2={a2:.1e} tol={tol:.1e} {'ok' if ok else 'FAIL'}",
               flush=True)
         del eng
     print(f"{cases} cases, {bad} failures, worst A2 {worst:.2e}, {time.time() - t0:.0f} s")
