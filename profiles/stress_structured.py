@@ -6,7 +6,7 @@ GPI2.GPI layers + MS(0,0,1/4) pairs; VQ: RX.RY.RZ + CNOT pairs + ZZ), the number
 entangler pattern (even / odd ladders, ring, chain, random explicit pairs) and the role of every
 parametrised layer (trainable / encoding / fixed), runs forward + adjoint through the engine at that
 tiling and compares <Z_q> (1e-5 absolute) and all angle gradients (A2, 1e-4) with the numpy oracle.
-usage: python profiles/stress_structured.py [CASES] [SEED]"""
+usage: python profiles/stress_structured.py [CASES] [SEED] [NMIN NMAX [MMIN MMAX]]   (half-open ranges)"""
 import os
 import sys
 import time
@@ -80,17 +80,22 @@ def build(n):
     return fam, Circuit(n, layers)
 
 
+N_RANGE, M_RANGE = (9, 15), (7, 12)  # n in [9, 15), M in [7, min(n, 12)); main() may widen them
+
+
 def draw_case():
     """(family, circuit, n, tile exponent M, batch) of the next random case"""
-    n = int(rng.integers(9, 15))
-    M = int(rng.integers(7, min(n, 12)))
+    n = int(rng.integers(*N_RANGE))
+    M = int(rng.integers(M_RANGE[0], min(n, M_RANGE[1])))
     fam, circ = build(n)
     return fam, circ, n, M, int(rng.integers(1, 4))
 
 
-def main(cases, seed):
-    global rng
+def main(cases, seed, n_range=None, m_range=None):
+    global rng, N_RANGE, M_RANGE
     from paper_2506_04891_b200.engine import Engine
+
+    N_RANGE, M_RANGE = n_range or N_RANGE, m_range or M_RANGE
 
     rng = np.random.default_rng(seed)
     worst, bad, t0 = 0.0, 0, time.time()
@@ -131,4 +136,6 @@ def main(cases, seed):
 
 
 if __name__ == "__main__":
-    sys.exit(main(int(sys.argv[1]) if len(sys.argv) > 1 else 40, int(sys.argv[2]) if len(sys.argv) > 2 else 0))
+    a = [int(v) for v in sys.argv[1:]]
+    sys.exit(main(a[0] if a else 40, a[1] if len(a) > 1 else 0,
+                  (a[2], a[3]) if len(a) > 3 else None, (a[4], a[5]) if len(a) > 5 else None))
