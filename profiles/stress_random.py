@@ -4,7 +4,7 @@ case: <Z_q> 1e-5 absolute; gradients A2 at 1e-4, or twice the A2 error of the re
 run in complex64 where that precision model itself breaks 1e-4 (the rule of
 tests/test_gpu_parity.py::test_random_circuits_multipass); structurally zero gradients absolutely
 (1e-6, or twice the complex64 model's own noise on them).
-usage: python profiles/stress_random.py [CASES] [SEED]"""
+usage: python profiles/stress_random.py [CASES] [SEED] [NMIN NMAX [MMIN]]   (n in [NMIN, NMAX), M in [MMIN, min(n, 13)])"""
 import os
 import sys
 import time
@@ -24,14 +24,14 @@ def a2(g, gr):
     return float(np.max(np.abs(g - gr) / np.maximum(np.abs(gr), 1e-2 * np.abs(gr).max())))
 
 
-def main(cases, seed):
+def main(cases, seed, n_range=(6, 13), m_min=5):
     from paper_2506_04891_b200.engine import Engine
 
     rng = np.random.default_rng(seed)
     bad, worst, t0 = 0, 0.0, time.time()
     for c in range(cases):
-        n = int(rng.integers(6, 13))
-        M = int(rng.integers(5, n + 1))
+        n = int(rng.integers(*n_range))
+        M = int(rng.integers(m_min, min(n, 13) + 1))
         circ = random_circuit(rng, n, int(rng.integers(6, 18)))
         B = int(rng.integers(1, 4))
         theta = rng.uniform(-3, 3, circ.trainable_count)
@@ -66,4 +66,6 @@ def main(cases, seed):
 
 
 if __name__ == "__main__":
-    sys.exit(main(int(sys.argv[1]) if len(sys.argv) > 1 else 40, int(sys.argv[2]) if len(sys.argv) > 2 else 0))
+    a = [int(v) for v in sys.argv[1:]]
+    sys.exit(main(a[0] if a else 40, a[1] if len(a) > 1 else 0, (a[2], a[3]) if len(a) > 3 else (6, 13),
+                  a[4] if len(a) > 4 else 5))
